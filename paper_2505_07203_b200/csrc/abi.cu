@@ -1,0 +1,50 @@
+// extern "C" surface of libprefillonly.so (declared in include/prefillonly.h).
+#include "../../include/prefillonly.h"
+#include "gemm.cuh"
+#include <cstdio>
+#include <string>
+#include <cstdarg>
+
+namespace po {
+thread_local std::string g_last_error;
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+}  // namespace po
+
+extern "C" {
+
+const char* po_last_error(void) { return po::g_last_error.c_str(); }
+const char* po_version(void) { return "prefillonly-b200 0.1 (sm_100a)"; }
+
+int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out, int64_t ldo, float* resid,
+               int64_t ldr, int32_t M, int32_t N, int32_t K, int32_t epi, const void* rope_table,
+               int32_t pos_offset, int32_t rope_cols, void* stream) {
+  if (!A || !B) return po::set_error(PO_ERR_ARG, "po_op_gemm: null operand");
+  if (M <= 0 || N % 256 || K % 64 || K <= 0 || N <= 0)
+    return po::set_error(PO_ERR_ARG, "po_op_gemm: need M>0, N%%256==0, K%%64==0 (got %d,%d,%d)", M, N, K);
+  if (epi == PO_EPI_RESID_F32 ? !resid : !out) return po::set_error(PO_ERR_ARG, "po_op_gemm: null output");
+  if (epi == PO_EPI_QKV_ROPE && !rope_table) return po::set_error(PO_ERR_ARG, "po_op_gemm: null rope table");
+  po::GemmPlan plan;
+  int rc = po::gemm_plan(&plan, A, lda, B, ldb, M, N, K);
+  if (rc) return po::set_error(PO_ERR_CUDA, "po_op_gemm: tensor map encode failed (%d)", rc);
+  po::GemmArgs args{};
+  args.out = out;
+  args.ldo = ldo;
+  args.resid = resid;
+  args.ldr = ldr;
+  args.rope = static_cast<const float2*>(rope_table);
+  args.pos_offset = pos_offset;
+  args.rope_cols = rope_cols;
+  rc = po::gemm_run(plan, epi, args, static_cast<cudaStream_t>(stream));
+  if (rc) return po::set_error(PO_ERR_CUDA, "po_op_gemm: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return PO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+// tcgen05 GEMM for sm_100a. See gemm.cuh for the contract.
+//
+// CTA layout (256 threads, 1 CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer (one lane): A 128x64 + B 256x64 bf16 per stage, 128B swizzle
+//   warp 1      MMA issuer (one lane): 4 x tcgen05.mma M128 N256 K16 per stage into a TMEM accumulator
+//   warp 2      TMEM allocator (512 columns = two 256-column accumulators, double buffered)
+//   warps 4..7  epilogue: tcgen05.ld 32 rows x 32 columns per warp, fused op, global store
+// Pipelines: smem full/empty ring (TMA <-> MMA) and TMEM full/empty pair (MMA <-> epilogue).
+#include "gemm.cuh"
+#include <cudaTypedefs.h>
+#include <cstdio>
+
+namespace po {
+
+namespace {
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KB
+constexpr int B_BYTES = BN * BK * 2;            // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
+constexpr int NUM_THREADS = 256;
+constexpr int GROUP_M = 16;                     // tile raster: 16 m-blocks share each n sweep
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+}  // namespace
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
+  const int per_group = GROUP_M * num_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  const int gsz = min(num_m - first_m, GROUP_M);
+  const int local = t - g * per_group;
+  m_blk = first_m + local % gsz;
+  n_blk = local / gsz;
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int col0, const uint32_t (&r)[32]) {
+  if constexpr (EPI == EPI_BF16) {
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 v;
+      v.x = pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1]));
+      v.y = pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
+      v.z = pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
+      v.w = pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
+      dst[q] = v;
+    }
+  } else if constexpr (EPI == EPI_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.out) + (long long)row * a.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                           __uint_as_float(r[4 * q + 3]));
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    float4* dst = reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 v = dst[q];
+      v.x += __uint_as_float(r[4 * q + 0]);
+      v.y += __uint_as_float(r[4 * q + 1]);
+      v.z += __uint_as_float(r[4 * q + 2]);
+      v.w += __uint_as_float(r[4 * q + 3]);
+      dst[q] = v;
+    }
+  } else if constexpr (EPI == EPI_SILU_MUL) {
+    // 32 accumulator columns = 16 gate columns followed by the matching 16 up columns.
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col0 / 2);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 8 * q + 2 * e;
+        const float x0 = silu_f(__uint_as_float(r[j])) * __uint_as_float(r[16 + j]);
+        const float x1 = silu_f(__uint_as_float(r[j + 1])) * __uint_as_float(r[16 + j + 1]);
+        w[e] = pack_bf16(x0, x1);
+      }
+      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = args.N / BN;
+  const int num_tiles = num_m * num_n;
+  const int nk = args.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
+          tma_load_2d(sA + s * A_BYTES, &map_a, &full_bar[s], kb * BK, mb * BM);
+          tma_load_2d(sB + s * B_BYTES, &map_b, &full_bar[s], kb * BK, nb * BN);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_ph = (it >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint64_t adesc = sdesc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
+          const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advance 16 bf16 = 32 bytes along K inside the swizzle atom (descriptor units of 16 B)
+            mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty_bar[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        mma_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wq = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_ph = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const int row = mb * BM + wq * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+      if constexpr (EPI == EPI_QKV_ROPE) {
+        // two 128-column heads per tile; rotate-half pairs (i, i+64)
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int hcol = nb * BN + h * 128;
+          const bool rot = hcol < args.rope_cols;
+          const float2* cs = args.rope + (long long)(args.pos_offset + row) * 64;
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            uint32_t x1[32], x2[32];
+            tmem_ld32(taddr + h * 128 + half * 32, x1);
+            tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
+            tmem_ld_wait();
+            if (row < args.M) {
+              if (rot) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const float2 c = cs[half * 32 + i];
+                  const float a0 = __uint_as_float(x1[i]);
+                  const float b0 = __uint_as_float(x2[i]);
+                  x1[i] = __float_as_uint(a0 * c.x - b0 * c.y);
+                  x2[i] = __float_as_uint(b0 * c.x + a0 * c.y);
+                }
+              }
+              epilogue_chunk<EPI_BF16>(args, row, hcol + half * 32, x1);
+              epilogue_chunk<EPI_BF16>(args, row, hcol + 64 + half * 32, x2);
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_ld_wait();
+          if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BN + c, r);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                      uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K) {
+  if (M <= 0 || N % BN != 0 || K % BK != 0) return -3;
+  plan->M = M;
+  plan->N = N;
+  plan->K = K;
+  if (make_tmap_2d_bf16(&plan->map_a, A, K, M, lda * 2, BK, BM)) return -2;
+  if (make_tmap_2d_bf16(&plan->map_b, B, K, N, ldb * 2, BK, BN)) return -2;
+  return 0;
+}
+
+template <int EPI>
+static int launch(const GemmPlan& plan, const GemmArgs& args, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    configured = true;
+  }
+  const int tiles = ((args.M + BM - 1) / BM) * (args.N / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_kernel<EPI><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(plan.map_a, plan.map_b, args);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t stream) {
+  GemmArgs args = in;
+  args.M = plan.M;
+  args.N = plan.N;
+  args.K = plan.K;
+  switch (epi) {
+    case EPI_BF16: return launch<EPI_BF16>(plan, args, stream);
+    case EPI_RESID_F32: return launch<EPI_RESID_F32>(plan, args, stream);
+    case EPI_SILU_MUL: return launch<EPI_SILU_MUL>(plan, args, stream);
+    case EPI_QKV_ROPE: return launch<EPI_QKV_ROPE>(plan, args, stream);
+    case EPI_F32: return launch<EPI_F32>(plan, args, stream);
+    default: return -3;
+  }
+}
+
+}  // namespace po

@@ -1,0 +1,39 @@
+// Persistent warp-specialised tcgen05 GEMM: D[M,N] = A[M,K] . B[N,K]^T (both K-major bf16), FP32
+// accumulation in TMEM, TMA loads through an mbarrier ring, fused epilogues for the PrefillOnly layer:
+//   EPI_BF16       plain bf16 store                      (generic)
+//   EPI_RESID_F32  resid[m,n] += acc (fp32, in place)    (O-proj and down-proj + residual)
+//   EPI_SILU_MUL   act = silu(gate) * up, gate/up interleaved in 16-column groups (ps/numerics.py:123-124,168)
+//   EPI_QKV_ROPE   RoPE (rotate-half, per 128-wide head) on q/k columns, bf16 store of the qkv row
+//   EPI_F32        plain fp32 store                      (tests / LM head)
+#pragma once
+#include "sm100.cuh"
+
+namespace po {
+
+enum GemmEpi : int { EPI_BF16 = 0, EPI_RESID_F32 = 1, EPI_SILU_MUL = 2, EPI_QKV_ROPE = 3, EPI_F32 = 4 };
+
+struct GemmArgs {
+  int M, N, K;
+  void* out;            // bf16 or fp32 output (EPI_BF16 / EPI_SILU_MUL / EPI_QKV_ROPE / EPI_F32)
+  long long ldo;        // elements
+  float* resid;         // EPI_RESID_F32
+  long long ldr;
+  const float2* rope;   // [pos][64] (cos, sin) for EPI_QKV_ROPE
+  int pos_offset;       // absolute position of row 0
+  int rope_cols;        // columns [0, rope_cols) are rotated (q and k heads)
+};
+
+struct GemmPlan {
+  CUtensorMap map_a;
+  CUtensorMap map_b;
+  int M, N, K;
+};
+
+// Host helpers (gemm.cu)
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                      uint32_t box_inner, uint32_t box_outer);
+int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K);
+int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& args, cudaStream_t stream);
+int num_sms();
+
+}  // namespace po
