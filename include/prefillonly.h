@@ -50,6 +50,13 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
                int64_t ldr, int32_t M, int32_t N, int32_t K, int32_t epi, const void* rope_table,
                int32_t pos_offset, int32_t rope_cols, void* stream);
 
+/* Causal GQA attention over one layer's qkv buffer (bf16 [n_total, ld]: Q | K | V columns, head_dim 128).
+ * Rows [0, q_offset) are cached-prefix rows that act only as keys; the output ctx (bf16 [n_total-q_offset,
+ * ldo]) holds the n_total-q_offset query rows. Replaces _attention (ps/numerics.py:132-146) generalised to
+ * GQA with prefix hits ((n^2 - n_c^2)/2 pairs, ps/costs.py:275-277). n_heads/n_kv_heads must be even. */
+int po_op_attention(const void* qkv, int64_t ld, int32_t n_total, int32_t q_offset, int32_t n_heads,
+                    int32_t n_kv_heads, void* out, int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

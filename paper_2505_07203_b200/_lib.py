@@ -44,6 +44,7 @@ _I64 = ctypes.c_int64
 SIGNATURES = {
     "po_last_error": (ctypes.c_char_p, []),
     "po_version": (ctypes.c_char_p, []),
+    "po_op_attention": (_I32, [_VP, _I64, _I32, _I32, _I32, _I32, _VP, _I64, _VP]),
     "po_op_gemm": (_I32, [_VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP, _I32, _I32, _VP]),
 }
 

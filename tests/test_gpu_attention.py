@@ -1,0 +1,79 @@
+"""tcgen05 causal GQA attention (po_op_attention) vs an fp32 torch reference of _attention.
+
+Reference semantics: ps/numerics.py:132-146 (scale 1/sqrt(d), triu mask, max-subtract softmax),
+generalised to GQA heads and a q_offset (cached-prefix rows act only as keys, ps/costs.py:275-277).
+Tolerance: P is rounded to bf16 before the PV product and the output is bf16 -> 2e-2 relative.
+"""
+
+import ctypes
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2505_07203_b200 import _lib  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def ref_attention(qkv, n_total, q_offset, hq, hkv):
+    hd = 128
+    x = qkv.float()
+    q = x[q_offset:, : hq * hd].view(-1, hq, hd)
+    k = x[:, hq * hd:(hq + hkv) * hd].view(n_total, hkv, hd)
+    v = x[:, (hq + hkv) * hd:(hq + 2 * hkv) * hd].view(n_total, hkv, hd)
+    g = hq // hkv
+    k = k.repeat_interleave(g, dim=1)
+    v = v.repeat_interleave(g, dim=1)
+    s = torch.einsum("qhd,khd->hqk", q, k) / hd ** 0.5
+    pos = torch.arange(q_offset, n_total, device=qkv.device)
+    keys = torch.arange(n_total, device=qkv.device)
+    s = s.masked_fill(keys[None, None, :] > pos[None, :, None], float("-inf"))
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hqk,khd->qhd", p, v).reshape(n_total - q_offset, hq * hd)
+
+
+def run(n_total, q_offset, hq, hkv, scale=1.0, seed=0):
+    torch.manual_seed(seed)
+    ld = (hq + 2 * hkv) * 128
+    qkv = (torch.randn(n_total, ld, device="cuda") * scale).to(torch.bfloat16)
+    out = torch.full((n_total - q_offset, hq * 128), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.call("po_op_attention", _p(qkv), ld, n_total, q_offset, hq, hkv, _p(out), hq * 128, None)
+    torch.cuda.synchronize()
+    ref = ref_attention(qkv, n_total, q_offset, hq, hkv)
+    err = ((out.float() - ref).norm() / ref.norm()).item()
+    return out, ref, err
+
+
+@pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (100, 2, 1), (128, 2, 1), (129, 4, 2), (1000, 8, 2),
+                                      (2048, 2, 1), (3000, 32, 8)])
+def test_attention_cold(n, hq, hkv):
+    out, ref, err = run(n, 0, hq, hkv, seed=n)
+    assert torch.isfinite(out.float()).all()
+    assert err < TOL, err
+
+
+@pytest.mark.parametrize("n,off", [(300, 16), (1000, 992), (2000, 1040), (4096, 4095), (1500, 128)])
+def test_attention_prefix_offset(n, off):
+    out, ref, err = run(n, off, 8, 2, seed=n + off)
+    assert torch.isfinite(out.float()).all()
+    assert err < TOL, err
+
+
+def test_attention_large_logits_rescale():
+    # large-magnitude scores force running-max updates (the stale-max rescale path)
+    out, ref, err = run(1500, 0, 4, 2, scale=4.0, seed=5)
+    assert torch.isfinite(out.float()).all()
+    assert err < TOL, err
+
+
+def test_attention_rejects_odd_group():
+    qkv = torch.zeros(16, 5 * 128, dtype=torch.bfloat16, device="cuda")
+    out = torch.zeros(16, 3 * 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(_lib.PrefillOnlyError):
+        _lib.call("po_op_attention", _p(qkv), 5 * 128, 16, 0, 3, 1, _p(out), 3 * 128, None)
