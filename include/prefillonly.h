@@ -57,6 +57,64 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
 int po_op_attention(const void* qkv, int64_t ld, int32_t n_total, int32_t q_offset, int32_t n_heads,
                     int32_t n_kv_heads, void* out, int64_t ldo, void* stream);
 
+/* ------------------------------------------------------------------------------------------------
+ * Engine (one per GPU; one request in flight, ps/sim.py:4-9). Replaces the engine slot
+ * execute_time(variant, geom, gpu, params, n_input, n_cached) called from sim.run.start_next
+ * (ps/costs.py:259-280, ps/sim.py:217-220): instead of returning modelled seconds, po_prefill runs the
+ * hybrid-prefill forward and the allowed-row LM head and reports measured device time.
+ * ------------------------------------------------------------------------------------------------ */
+typedef struct po_model_cfg {
+  int32_t num_layers;        /* ModelGeometry.num_layers            (ps/geometry.py:29-33)              */
+  int32_t hidden;            /* ModelGeometry.hidden_size                                               */
+  int32_t n_heads;           /* query heads (absent in reference; Llama config)                        */
+  int32_t n_kv_heads;        /* ModelGeometry.num_kv_heads                                              */
+  int32_t head_dim;          /* ModelGeometry.head_dim (must be 128)                                    */
+  int32_t intermediate;      /* ModelGeometry.intermediate_size                                         */
+  int32_t vocab;             /* vocabulary rows of embed / lm_head                                      */
+  float rms_eps;             /* RMSNorm epsilon                                                         */
+  float rope_theta;          /* RoPE base                                                               */
+  int32_t rope_scaling;      /* 0 = none, 1 = llama3                                                    */
+  float rope_factor, rope_low_freq_factor, rope_high_freq_factor;
+  int32_t rope_original_max_pos;
+  int32_t max_tokens;        /* largest request the arena serves (the MIL, ps/geometry.py:203-212)     */
+  int32_t chunk;             /* hybrid-prefill MLP chunk rows (DEFAULT_CHUNK = 8192, ps/geometry.py:14) */
+  int32_t block_tokens;      /* prefix-pool block (CacheConfig.block_tokens = 16, ps/cache.py:65-80)   */
+  int64_t pool_blocks;       /* prefix-pool capacity in blocks; < 0 = size by a profile run            */
+  double pool_mem_fraction;  /* profile run: fraction of HBM left after the arena given to the pool    */
+} po_model_cfg;
+
+typedef struct po_engine po_engine;
+
+/* Allocate weights (counter-hash random init from `seed`, bit-reproducible by oracle/), the activation
+ * arena for cfg->max_tokens, the one-layer K/V buffer and the prefix pool. */
+int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** out);
+int po_free(po_engine* e);
+
+/* One prefill-only request: tokens[n] (uint32 ids, embedded as id % vocab), n_cached prefix tokens already
+ * resident in the pool (multiple of block_tokens). pool_block_ids[b] for b < n_blocks: for cached blocks
+ * (b < n_cached/block_tokens) the slot holding block b; for later blocks the slot to admit block b into, or
+ * -1 (suffix discard, ps/cache.py:143-159). Outputs (host): logits/probs over the allowed ids (softmax
+ * restricted to them) and the argmax index into `allowed` (first maximum). PO_ERR_CAPACITY when
+ * n > max_tokens (CapacityError, ps/costs.py:270-274). */
+int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
+               int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
+               float* out_probs, int32_t* out_argmax, void* stream);
+
+/* Device milliseconds of the last po_prefill (CUDA events around the forward on the engine stream). */
+int po_last_service_ms(po_engine* e, float* ms);
+
+/* Drop pool slots (metadata-only: slots are overwritten on reuse; validates the ids). */
+int po_pool_evict(po_engine* e, const int32_t* slots, int32_t n);
+
+/* Engine facts: [0] pool_blocks, [1] weight bytes, [2] arena bytes, [3] pool bytes, [4] bytes per pool block,
+ * [5] max_tokens, [6] device free bytes after init. */
+int po_engine_info(po_engine* e, int64_t* out, int32_t n);
+
+/* Overwrite one weight tensor from host memory (logical, un-interleaved layout; bf16 except norms = fp32).
+ * kind: 0 embed, 1 attn_norm, 2 wq, 3 wk, 4 wv, 5 wo, 6 mlp_norm, 7 w_gate, 8 w_up, 9 w_down, 10 final_norm,
+ * 11 lm_head. */
+int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, int64_t nelem);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,266 @@
+"""CPU oracle for the PrefillOnly layer forward — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import this module, and only
+as the checker / CPU baseline; the product path (paper_2505_07203_b200/) never calls it.
+
+What it restates (numpy, float64 arithmetic):
+  * the reference toy block (ps/numerics.py:132-171): `toy_block_forward` = block_forward_full, built
+    from the same helpers the Llama forward uses (`causal_attention`, `gated_mlp`). It is PINNED against
+    the reference: <= 1e-12 vs block_forward_full and the SEED42 sha256 fixture
+    (pkg/tests/test_numerics.py:18,86-90), see tests/test_oracle_numerics.py.
+  * the Llama-style block the B200 engine runs (embedding, RMSNorm, RoPE, GQA, residuals, allowed-row LM
+    head). The reference has none of these: parity for them is UNPINNED by the reference
+    and rests on the definitions stated here and in DESIGN.md, cross-checked against transformers' Llama.
+  * the engine's counter-hash weight init, bit for bit (csrc/kernels.cu: unit_uniform / init kernels).
+
+bf16-faithful: values are rounded to bf16 at the same storage points as the kernels (normed activations,
+roped q/k, v, attention output, SiLU.mul output, final hidden); accumulation is float64.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+# ------------------------------------------------------------------ bf16 and the counter hash
+
+K_SEED = np.uint64(0x9E3779B97F4A7C15)
+K_TID = np.uint64(0xD1B54A32D192ED03)
+SQRT3_F32 = np.float32(1.7320508)
+TID_EMBED, TID_FINAL_NORM, TID_LM_HEAD = 0xFFFF0, 0xFFFF1, 0xFFFF2
+K_ATTN_NORM, K_Q, K_K, K_V, K_O, K_MLP_NORM, K_GATE, K_UP, K_DOWN = range(9)
+
+
+def bf16_round(x) -> np.ndarray:
+    """Round float32 values to the nearest bf16 (ties to even); returns float32 holding bf16 values."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    bits = a.view(np.uint32).astype(np.uint64)
+    rounded = ((bits + np.uint64(0x7FFF) + ((bits >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
+    return rounded.astype(np.uint32).view(np.float32).reshape(a.shape)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def unit_uniform(seed: int, tid: int, idx: np.ndarray) -> np.ndarray:
+    """Counter-based U[-sqrt3, sqrt3) in float32, identical to csrc/kernels.cu:unit_uniform."""
+    with np.errstate(over="ignore"):
+        key = np.uint64(seed) * K_SEED + np.uint64(tid) * K_TID + idx.astype(np.uint64)
+    z = splitmix64(key)
+    u = (z >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0)
+    return ((np.float32(2.0) * u - np.float32(1.0)) * SQRT3_F32).astype(np.float32)
+
+
+def fan_scale(fan_in: int) -> np.float32:
+    return np.float32(1.0 / np.sqrt(np.float64(fan_in)))
+
+
+def init_matrix(seed: int, tid: int, rows: int, cols: int, scale) -> np.ndarray:
+    """bf16 weight [rows, cols] (as float32) = bf16(u * scale) (init_bf16_kernel, INIT_PLAIN)."""
+    out = np.empty((rows, cols), dtype=np.float32)
+    step = max(1, (1 << 22) // cols)
+    for r0 in range(0, rows, step):
+        r1 = min(rows, r0 + step)
+        idx = np.arange(r0 * cols, r1 * cols, dtype=np.uint64)
+        out[r0:r1] = bf16_round(unit_uniform(seed, tid, idx) * np.float32(scale)).reshape(r1 - r0, cols)
+    return out
+
+
+def init_norm(seed: int, tid: int, n: int) -> np.ndarray:
+    u = unit_uniform(seed, tid, np.arange(n, dtype=np.uint64))
+    return bf16_round(np.float32(1.0) + np.float32(0.05) * u)
+
+
+def layer_tid(layer: int, kind: int) -> int:
+    return layer * 16 + kind
+
+
+# ------------------------------------------------------------------ configuration and weights
+
+
+@dataclass(frozen=True)
+class Cfg:
+    num_layers: int
+    hidden: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    intermediate: int
+    vocab: int
+    rms_eps: float = 1e-5
+    rope_theta: float = 500_000.0
+    rope_scaling: int = 1
+    rope_factor: float = 8.0
+    rope_low_freq_factor: float = 1.0
+    rope_high_freq_factor: float = 4.0
+    rope_original_max_pos: int = 8192
+
+    @classmethod
+    def from_model(cls, m) -> "Cfg":
+        return cls(**{k: getattr(m, k) for k in cls.__dataclass_fields__})
+
+
+def make_weights(cfg: Cfg, seed: int) -> dict:
+    """All weights as float32 arrays holding bf16 values, in the logical (un-interleaved) layout."""
+    h, i_, hd = cfg.hidden, cfg.intermediate, cfg.head_dim
+    w = {
+        "embed": init_matrix(seed, TID_EMBED, cfg.vocab, h, np.float32(1.0)),
+        "lm_head": init_matrix(seed, TID_LM_HEAD, cfg.vocab, h, fan_scale(h)),
+        "final_norm": init_norm(seed, TID_FINAL_NORM, h),
+        "layers": [],
+    }
+    for l in range(cfg.num_layers):
+        w["layers"].append({
+            "attn_norm": init_norm(seed, layer_tid(l, K_ATTN_NORM), h),
+            "wq": init_matrix(seed, layer_tid(l, K_Q), cfg.n_heads * hd, h, fan_scale(h)),
+            "wk": init_matrix(seed, layer_tid(l, K_K), cfg.n_kv_heads * hd, h, fan_scale(h)),
+            "wv": init_matrix(seed, layer_tid(l, K_V), cfg.n_kv_heads * hd, h, fan_scale(h)),
+            "wo": init_matrix(seed, layer_tid(l, K_O), h, cfg.n_heads * hd, fan_scale(cfg.n_heads * hd)),
+            "mlp_norm": init_norm(seed, layer_tid(l, K_MLP_NORM), h),
+            "w_gate": init_matrix(seed, layer_tid(l, K_GATE), i_, h, fan_scale(h)),
+            "w_up": init_matrix(seed, layer_tid(l, K_UP), i_, h, fan_scale(h)),
+            "w_down": init_matrix(seed, layer_tid(l, K_DOWN), h, i_, fan_scale(i_)),
+        })
+    return w
+
+
+# ------------------------------------------------------------------ shared block pieces
+
+
+def silu(z: np.ndarray) -> np.ndarray:
+    """z / (1 + e^-z)  (ps/numerics.py:123-124)."""
+    return z / (1.0 + np.exp(-z))
+
+
+def causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_offset: int = 0) -> np.ndarray:
+    """Causal softmax(q k^T / sqrt(d)) v per head, GQA by head grouping (ps/numerics.py:132-146).
+
+    q: (n_q, Hq, d); k, v: (n_kv, Hkv, d); query row r sits at position q_offset + r and attends to keys
+    0..q_offset+r (the triu mask of the reference shifted by the cached prefix).
+    """
+    n_q, hq, d = q.shape
+    n_kv, hkv, _ = k.shape
+    group = hq // hkv
+    pos = np.arange(q_offset, q_offset + n_q)
+    keys = np.arange(n_kv)
+    masked = keys[None, :] > pos[:, None]
+    out = np.empty((n_q, hq, d), dtype=np.float64)
+    for hh in range(hq):
+        kh = k[:, hh // group, :].astype(np.float64)
+        vh = v[:, hh // group, :].astype(np.float64)
+        s = (q[:, hh, :].astype(np.float64) @ kh.T) / np.sqrt(d)
+        s[masked] = -np.inf
+        s -= s.max(axis=1, keepdims=True)
+        np.exp(s, out=s)
+        s /= s.sum(axis=1, keepdims=True)
+        out[:, hh, :] = s @ vh
+    return out
+
+
+def gated_mlp(x: np.ndarray, w_gate: np.ndarray, w_up: np.ndarray, w_down: np.ndarray, round_act=False):
+    """silu(x Wg) * (x Wu) then Wd, weights given as [in, out] (ps/numerics.py:165-170)."""
+    g = x @ w_gate
+    u = x @ w_up
+    act = silu(g) * u
+    if round_act:
+        act = bf16_round(act).astype(np.float64)
+    return act @ w_down
+
+
+# ------------------------------------------------------------------ reference toy block (pinned)
+
+
+def toy_block_forward(w_qkv: np.ndarray, w_out: np.ndarray, w_gate_up: np.ndarray, w_down: np.ndarray,
+                      x: np.ndarray) -> np.ndarray:
+    """block_forward_full (ps/numerics.py:149-171): single-head causal attention + SiLU-gated MLP.
+
+    Weights in the reference's [in, out] layout; [q|k|v] and [gate|up] column splits (:143, :168).
+    """
+    h = w_qkv.shape[0]
+    inter = w_down.shape[0]
+    qkv = x @ w_qkv
+    q, k, v = qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:]
+    ctx = causal_attention(q[:, None, :], k[:, None, :], v[:, None, :])[:, 0, :]
+    attn = ctx @ w_out
+    return gated_mlp(attn, w_gate_up[:, :inter], w_gate_up[:, inter:], w_down)
+
+
+# ------------------------------------------------------------------ Llama block (engine semantics)
+
+
+def rope_inv_freq(cfg: Cfg) -> np.ndarray:
+    """Llama-3 RoPE inverse frequencies, float64 then rounded once to float32 (engine.cu:rope_inv_freq)."""
+    i = np.arange(cfg.head_dim // 2, dtype=np.float64)
+    f = 1.0 / np.power(np.float64(np.float32(cfg.rope_theta)), 2.0 * i / cfg.head_dim)
+    if cfg.rope_scaling == 1:
+        factor = np.float64(np.float32(cfg.rope_factor))
+        low = np.float64(np.float32(cfg.rope_low_freq_factor))
+        high = np.float64(np.float32(cfg.rope_high_freq_factor))
+        orig = np.float64(cfg.rope_original_max_pos)
+        low_wl, high_wl = orig / low, orig / high
+        wl = 2.0 * np.pi / f
+        smooth = (orig / wl - low) / (high - low)
+        mid = (1.0 - smooth) * f / factor + smooth * f
+        f = np.where(wl > low_wl, f / factor, np.where(wl >= high_wl, mid, f))
+    return f.astype(np.float32)
+
+
+def rope_table(cfg: Cfg, n: int) -> tuple[np.ndarray, np.ndarray]:
+    inv = rope_inv_freq(cfg)
+    ang = np.arange(n, dtype=np.float32)[:, None] * inv[None, :]  # float32 product
+    a64 = ang.astype(np.float64)
+    return np.cos(a64).astype(np.float32), np.sin(a64).astype(np.float32)
+
+
+def rmsnorm(x: np.ndarray, gamma: np.ndarray, eps: float) -> np.ndarray:
+    ms = np.mean(x * x, axis=-1, keepdims=True)
+    return bf16_round((x / np.sqrt(ms + eps)) * gamma).astype(np.float64)
+
+
+def apply_rope(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
+    """Rotate-half RoPE on (n, H, d): pairs (i, i + d/2)."""
+    half = x.shape[-1] // 2
+    c = cos[:, None, :].astype(np.float64)
+    s = sin[:, None, :].astype(np.float64)
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_hidden: bool = False):
+    """Prefill-only forward of one request; returns (logits, probs, argmax) over the allowed ids.
+
+    Cached-prefix rows only serve as keys; their K/V equal what a cold forward computes (causality), so the
+    oracle computes them directly. Layer semantics follow engine.cu's header comment.
+    """
+    toks = np.asarray(tokens, dtype=np.uint64) % np.uint64(cfg.vocab)
+    n = len(toks)
+    hd, hq, hkv = cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
+    cos, sin = rope_table(cfg, n)
+    x = w["embed"][toks.astype(np.int64)].astype(np.float64)
+    for lw in w["layers"]:
+        xn = rmsnorm(x, lw["attn_norm"], cfg.rms_eps)
+        q = (xn @ lw["wq"].T.astype(np.float64)).reshape(n, hq, hd)
+        k = (xn @ lw["wk"].T.astype(np.float64)).reshape(n, hkv, hd)
+        v = (xn @ lw["wv"].T.astype(np.float64)).reshape(n, hkv, hd)
+        q = bf16_round(apply_rope(q, cos, sin)).astype(np.float64)
+        k = bf16_round(apply_rope(k, cos, sin)).astype(np.float64)
+        v = bf16_round(v).astype(np.float64)
+        ctx = bf16_round(causal_attention(q, k, v)).astype(np.float64).reshape(n, hq * hd)
+        x = x + ctx @ lw["wo"].T.astype(np.float64)
+        xn2 = rmsnorm(x, lw["mlp_norm"], cfg.rms_eps)
+        x = x + gated_mlp(xn2, lw["w_gate"].T.astype(np.float64), lw["w_up"].T.astype(np.float64),
+                          lw["w_down"].T.astype(np.float64), round_act=True)
+    h_last = rmsnorm(x[-1:], w["final_norm"], cfg.rms_eps)[0]
+    alw = np.asarray(allowed, dtype=np.int64)
+    logits = w["lm_head"][alw].astype(np.float64) @ h_last
+    e = np.exp(logits - logits.max())
+    probs = e / e.sum()
+    if return_hidden:
+        return logits, probs, int(np.argmax(logits)), x
+    return logits, probs, int(np.argmax(logits))

@@ -44,6 +44,13 @@ _I64 = ctypes.c_int64
 SIGNATURES = {
     "po_last_error": (ctypes.c_char_p, []),
     "po_version": (ctypes.c_char_p, []),
+    "po_init": (_I32, [_I32, _VP, ctypes.c_uint64, _VP]),
+    "po_free": (_I32, [_VP]),
+    "po_prefill": (_I32, [_VP, _VP, _I32, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
+    "po_last_service_ms": (_I32, [_VP, _VP]),
+    "po_pool_evict": (_I32, [_VP, _VP, _I32]),
+    "po_engine_info": (_I32, [_VP, _VP, _I32]),
+    "po_load_weight": (_I32, [_VP, _I32, _I32, _VP, _I64]),
     "po_op_attention": (_I32, [_VP, _I64, _I32, _I32, _I32, _I32, _VP, _I64, _VP]),
     "po_op_gemm": (_I32, [_VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP, _I32, _I32, _VP]),
 }

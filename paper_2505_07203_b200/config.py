@@ -1,0 +1,123 @@
+"""Model shapes and engine sizing.
+
+The reference's ModelGeometry (ps/geometry.py:26-57) and its presets
+(ps/presets/llama-3.1-8b.preset:7-15, qwen-32b-fp8.preset:7-16) carry only the byte-arithmetic
+fields. A real forward also needs query heads, vocabulary, RMSNorm epsilon and RoPE constants; those
+come from the public model configs and are stated here (parity for them is unpinned).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import asdict, dataclass, replace
+
+DEFAULT_CHUNK = 8192  # ps/geometry.py:14
+BLOCK_TOKENS = 16  # CacheConfig.block_tokens default, ps/cache.py:65-80
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    num_layers: int
+    hidden: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    intermediate: int
+    vocab: int
+    rms_eps: float = 1e-5
+    rope_theta: float = 500_000.0
+    rope_scaling: int = 1  # 0 none, 1 llama3
+    rope_factor: float = 8.0
+    rope_low_freq_factor: float = 1.0
+    rope_high_freq_factor: float = 4.0
+    rope_original_max_pos: int = 8192
+
+    @property
+    def kv_bytes_per_token(self) -> tuple[int, int]:
+        """(per-layer, all-layer) bf16 K/V bytes of one token (ps/geometry.py:147-150)."""
+        per_layer = 2 * self.n_kv_heads * self.head_dim * 2
+        return per_layer, per_layer * self.num_layers
+
+    @property
+    def weight_bytes(self) -> int:
+        h, i = self.hidden, self.intermediate
+        qkv = (self.n_heads + 2 * self.n_kv_heads) * self.head_dim * h
+        o = self.n_heads * self.head_dim * h
+        per_layer = qkv + o + 3 * h * i + 2 * h
+        return 2 * (self.num_layers * per_layer + 2 * self.vocab * h + h)
+
+    def linear_flops_per_token(self) -> float:
+        """Dense-layer FLOPs per token over all layers (ps/costs.py:126-131)."""
+        h = self.hidden
+        kv_dim = self.n_kv_heads * self.head_dim
+        per_layer = 2.0 * (h * (h + 2 * kv_dim) + h * h + 3 * h * self.intermediate)
+        return self.num_layers * per_layer
+
+    def attn_flops_per_pair(self) -> float:
+        """Attention FLOPs per (query, key) pair over all layers (ps/costs.py:134-136)."""
+        return 4.0 * self.hidden * self.num_layers
+
+    def request_flops(self, n: int, n_cached: int = 0, n_allowed: int = 2) -> float:
+        """Algorithmic FLOPs of one request: linear x miss + attn x (n^2 - n_c^2)/2 (ps/costs.py:275-277)."""
+        miss = n - n_cached
+        pairs = (n * n - n_cached * n_cached) / 2.0
+        return self.linear_flops_per_token() * miss + self.attn_flops_per_pair() * pairs + 2.0 * self.hidden * n_allowed
+
+
+# Llama-3.1-8B: meta-llama/Llama-3.1-8B config.json (rope_scaling llama3, factor 8, theta 5e5, eps 1e-5)
+LLAMA_3_1_8B = ModelConfig("llama-3.1-8b", 32, 4096, 32, 8, 128, 14336, 128_256)
+# Tiny parity config (BASELINE.json configs[0]): 2 layers, d=256, GQA 2:1, build-chosen and stated.
+TINY = ModelConfig("tiny", 2, 256, 2, 1, 128, 1024, 32_000)
+# Qwen-2.5-32B shapes (Qwen/Qwen2.5-32B config.json), rope theta 1e6, eps 1e-6, no rope scaling.
+# Note: 40 query / 8 kv heads is an odd GQA group (5); the attention kernel pairs heads within a group,
+# so this preset is declared for sizing and is rejected by po_init until odd groups are supported.
+QWEN_2_5_32B = ModelConfig("qwen-2.5-32b", 64, 5120, 40, 8, 128, 27648, 152_064, rms_eps=1e-6,
+                           rope_theta=1_000_000.0, rope_scaling=0)
+
+PRESETS = {c.name: c for c in (TINY, LLAMA_3_1_8B, QWEN_2_5_32B)}
+
+
+def get_preset(name: str) -> ModelConfig:
+    try:
+        return PRESETS[name]
+    except KeyError:
+        raise ValueError(f"unknown model preset {name!r}; known: {sorted(PRESETS)}") from None
+
+
+class PoModelCfg(ctypes.Structure):
+    """ctypes mirror of po_model_cfg (include/prefillonly.h)."""
+
+    _fields_ = [
+        ("num_layers", ctypes.c_int32),
+        ("hidden", ctypes.c_int32),
+        ("n_heads", ctypes.c_int32),
+        ("n_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("intermediate", ctypes.c_int32),
+        ("vocab", ctypes.c_int32),
+        ("rms_eps", ctypes.c_float),
+        ("rope_theta", ctypes.c_float),
+        ("rope_scaling", ctypes.c_int32),
+        ("rope_factor", ctypes.c_float),
+        ("rope_low_freq_factor", ctypes.c_float),
+        ("rope_high_freq_factor", ctypes.c_float),
+        ("rope_original_max_pos", ctypes.c_int32),
+        ("max_tokens", ctypes.c_int32),
+        ("chunk", ctypes.c_int32),
+        ("block_tokens", ctypes.c_int32),
+        ("pool_blocks", ctypes.c_int64),
+        ("pool_mem_fraction", ctypes.c_double),
+    ]
+
+
+def to_c_cfg(model: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK, block_tokens: int = BLOCK_TOKENS,
+             pool_blocks: int = -1, pool_mem_fraction: float = 0.9) -> PoModelCfg:
+    d = asdict(model)
+    d.pop("name")
+    return PoModelCfg(**d, max_tokens=max_tokens, chunk=chunk, block_tokens=block_tokens, pool_blocks=pool_blocks,
+                      pool_mem_fraction=pool_mem_fraction)
+
+
+__all__ = ["ModelConfig", "PoModelCfg", "to_c_cfg", "get_preset", "PRESETS", "TINY", "LLAMA_3_1_8B",
+           "QWEN_2_5_32B", "DEFAULT_CHUNK", "BLOCK_TOKENS", "replace"]

@@ -1,0 +1,449 @@
+// PrefillOnly engine: weights, activation arena, one-layer K/V buffer, prefix pool, hybrid-prefill forward.
+//
+// Forward of one request (n tokens, n_c cached, ps/numerics.py:215-275 generalised to Llama):
+//   resid = embed(tokens[n_c:])                                            fp32 [n_miss, h]
+//   for each layer:                                     (KV of this layer only: qkv is reused across layers)
+//     xn   = rmsnorm(resid) * g_attn                                       bf16 [n_miss, h]
+//     qkv[:n_c, kv]   = gather(prefix pool, cached blocks)                 bf16 K/V of the cached prefix
+//     qkv[n_c:]       = xn . Wqkv^T  (+RoPE epilogue)                      tcgen05 GEMM
+//     pool[admitted]  = qkv[admitted rows, kv]                             prefix-pool admission
+//     ctx  = causal GQA attention(qkv, q_offset = n_c)                     full length, tcgen05 FA
+//     resid += ctx . Wo^T                                                  residual epilogue, in place
+//     for chunk of rows:                                                   hybrid: MLP chunked
+//       xn[chunk]    = rmsnorm(resid[chunk]) * g_mlp
+//       act          = silu(xn Wg^T) * (xn Wu^T)                           one GEMM, SiLU.mul epilogue
+//       resid[chunk] += act . Wd^T                                         residual epilogue, in place
+//   logits over allowed ids = lm_head[allowed] . rmsnorm(resid[last]) * g_final
+#include "../../include/prefillonly.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace po {
+int set_error(int code, const char* fmt, ...);
+int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
+                  cudaStream_t stream);
+}  // namespace po
+
+struct po_engine {
+  po_model_cfg cfg;
+  int device = 0;
+  uint64_t seed = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // weights
+  __nv_bfloat16* embed = nullptr;
+  __nv_bfloat16* lm_head = nullptr;
+  float* final_norm = nullptr;
+  struct Layer {
+    __nv_bfloat16 *wqkv, *wo, *wgu, *wdown;
+    float *attn_norm, *mlp_norm;
+    CUtensorMap map_qkv, map_o, map_gu, map_down;
+  };
+  std::vector<Layer> layers;
+  // arena
+  float* resid = nullptr;
+  __nv_bfloat16* xn = nullptr;  // also the attention output (ctx)
+  __nv_bfloat16* qkv = nullptr;
+  __nv_bfloat16* act = nullptr;
+  float2* rope = nullptr;
+  CUtensorMap map_xn, map_ctx, map_act;
+  // per-request device staging
+  uint32_t* d_tokens = nullptr;
+  int* d_slots = nullptr;
+  int2* d_admit = nullptr;
+  int* d_allowed = nullptr;
+  float* d_logits = nullptr;
+  float* d_probs = nullptr;
+  int* d_argmax = nullptr;
+  // pinned host staging
+  uint32_t* h_tokens = nullptr;
+  int* h_slots = nullptr;
+  int2* h_admit = nullptr;
+  int* h_allowed = nullptr;
+  float* h_logits = nullptr;
+  float* h_probs = nullptr;
+  int* h_argmax = nullptr;
+  // prefix pool [slot][layer][block_tokens][kv_dim]
+  __nv_bfloat16* pool = nullptr;
+  int64_t pool_blocks = 0;
+  int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0;
+  std::vector<void*> allocs;
+  float last_ms = 0.f;
+
+  int qkv_cols() const { return (cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim; }
+  int kv_dim() const { return 2 * cfg.n_kv_heads * cfg.head_dim; }
+  int ctx_cols() const { return cfg.n_heads * cfg.head_dim; }
+  int64_t block_bytes() const { return (int64_t)cfg.num_layers * cfg.block_tokens * kv_dim() * 2; }
+};
+
+namespace {
+using po::set_error;
+
+// tensor ids of the counter-hash init (oracle/llama_ref.py mirrors these)
+constexpr uint32_t TID_EMBED = 0xFFFF0, TID_FINAL_NORM = 0xFFFF1, TID_LM_HEAD = 0xFFFF2;
+enum { K_ATTN_NORM = 0, K_Q = 1, K_K = 2, K_V = 3, K_O = 4, K_MLP_NORM = 5, K_GATE = 6, K_UP = 7, K_DOWN = 8 };
+inline uint32_t layer_tid(int layer, int kind) { return static_cast<uint32_t>(layer) * 16u + kind; }
+inline float fan_scale(int fan_in) { return static_cast<float>(1.0 / std::sqrt(static_cast<double>(fan_in))); }
+
+template <typename T>
+int dalloc(po_engine* e, T** p, size_t bytes, int64_t* counter) {
+  void* q = nullptr;
+  if (cudaMalloc(&q, bytes ? bytes : 16) != cudaSuccess) return -1;
+  e->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  if (counter) *counter += bytes;
+  return 0;
+}
+template <typename T>
+int halloc(T** p, size_t bytes) {
+  return cudaMallocHost(reinterpret_cast<void**>(p), bytes ? bytes : 16) == cudaSuccess ? 0 : -1;
+}
+
+// Llama-3 RoPE inverse frequencies in double, rounded once to fp32 (oracle/llama_ref.py: rope_inv_freq)
+std::vector<float> rope_inv_freq(const po_model_cfg& c) {
+  std::vector<float> out(c.head_dim / 2);
+  for (int i = 0; i < c.head_dim / 2; ++i) {
+    double f = 1.0 / std::pow(static_cast<double>(c.rope_theta), (2.0 * i) / c.head_dim);
+    if (c.rope_scaling == 1) {
+      const double orig = c.rope_original_max_pos;
+      const double low_wl = orig / c.rope_low_freq_factor, high_wl = orig / c.rope_high_freq_factor;
+      const double wl = 2.0 * M_PI / f;
+      if (wl > low_wl) {
+        f = f / c.rope_factor;
+      } else if (wl >= high_wl) {
+        const double s = (orig / wl - c.rope_low_freq_factor) / (c.rope_high_freq_factor - c.rope_low_freq_factor);
+        f = (1.0 - s) * f / c.rope_factor + s * f;
+      }
+    }
+    out[i] = static_cast<float>(f);
+  }
+  return out;
+}
+
+int validate_cfg(const po_model_cfg& c) {
+  if (c.num_layers <= 0 || c.hidden <= 0 || c.n_heads <= 0 || c.n_kv_heads <= 0 || c.intermediate <= 0 ||
+      c.vocab <= 0 || c.max_tokens <= 0 || c.chunk <= 0 || c.block_tokens <= 0)
+    return set_error(PO_ERR_CONFIG, "po_init: all shape counts must be positive");
+  if (c.head_dim != 128) return set_error(PO_ERR_CONFIG, "po_init: head_dim must be 128 (got %d)", c.head_dim);
+  if (c.n_heads % c.n_kv_heads || (c.n_heads / c.n_kv_heads) % 2)
+    return set_error(PO_ERR_CONFIG, "po_init: n_heads/n_kv_heads must be an even integer");
+  if (c.hidden % 256 || c.intermediate % 128 || ((c.n_heads + 2 * c.n_kv_heads) * 128) % 256)
+    return set_error(PO_ERR_CONFIG, "po_init: hidden %% 256, intermediate %% 128 and qkv width %% 256 required");
+  if (c.hidden > 8192) return set_error(PO_ERR_CONFIG, "po_init: hidden > 8192 unsupported by the LM-head kernel");
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int po_free(po_engine* e) {
+  if (!e) return PO_OK;
+  cudaSetDevice(e->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  for (void* p : e->allocs) cudaFree(p);
+  cudaFreeHost(e->h_tokens);
+  cudaFreeHost(e->h_slots);
+  cudaFreeHost(e->h_admit);
+  cudaFreeHost(e->h_allowed);
+  cudaFreeHost(e->h_logits);
+  cudaFreeHost(e->h_probs);
+  cudaFreeHost(e->h_argmax);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+  return PO_OK;
+}
+
+int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** out) {
+  if (!cfg || !out) return set_error(PO_ERR_ARG, "po_init: null argument");
+  *out = nullptr;
+  if (int rc = validate_cfg(*cfg)) return rc;
+  if (cudaSetDevice(device) != cudaSuccess) return set_error(PO_ERR_CUDA, "po_init: cudaSetDevice(%d) failed", device);
+  po_engine* e = new po_engine();
+  e->cfg = *cfg;
+  e->device = device;
+  e->seed = seed;
+  const po_model_cfg& c = e->cfg;
+  auto fail = [&](int code, const char* what) {
+    int rc = set_error(code, "po_init: %s (%s)", what, cudaGetErrorString(cudaGetLastError()));
+    po_free(e);
+    return rc;
+  };
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess)
+    return fail(PO_ERR_CUDA, "stream/event creation failed");
+  const int h = c.hidden, I = c.intermediate, L = c.num_layers;
+  const int qkvc = e->qkv_cols(), ctxc = e->ctx_cols();
+  const long long T = c.max_tokens;
+  cudaStream_t s = e->stream;
+
+  // ---- weights (counter-hash init; bf16, norms as fp32 holding bf16 values)
+  if (dalloc(e, &e->embed, (size_t)c.vocab * h * 2, &e->weight_bytes) ||
+      dalloc(e, &e->lm_head, (size_t)c.vocab * h * 2, &e->weight_bytes) ||
+      dalloc(e, &e->final_norm, (size_t)h * 4, &e->weight_bytes))
+    return fail(PO_ERR_CUDA, "weight allocation failed");
+  po::launch_init_bf16(e->embed, c.vocab, h, seed, TID_EMBED, 0, 1.0f, po::INIT_PLAIN, s);
+  po::launch_init_bf16(e->lm_head, c.vocab, h, seed, TID_LM_HEAD, 0, fan_scale(h), po::INIT_PLAIN, s);
+  po::launch_init_norm(e->final_norm, h, seed, TID_FINAL_NORM, s);
+  e->layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    auto& ly = e->layers[l];
+    if (dalloc(e, &ly.wqkv, (size_t)qkvc * h * 2, &e->weight_bytes) ||
+        dalloc(e, &ly.wo, (size_t)h * ctxc * 2, &e->weight_bytes) ||
+        dalloc(e, &ly.wgu, (size_t)2 * I * h * 2, &e->weight_bytes) ||
+        dalloc(e, &ly.wdown, (size_t)h * I * 2, &e->weight_bytes) ||
+        dalloc(e, &ly.attn_norm, (size_t)h * 4, &e->weight_bytes) ||
+        dalloc(e, &ly.mlp_norm, (size_t)h * 4, &e->weight_bytes))
+      return fail(PO_ERR_CUDA, "weight allocation failed");
+    const int qrows = c.n_heads * c.head_dim, kvrows = c.n_kv_heads * c.head_dim;
+    po::launch_init_bf16(ly.wqkv, qrows, h, seed, layer_tid(l, K_Q), 0, fan_scale(h), po::INIT_PLAIN, s);
+    po::launch_init_bf16(ly.wqkv + (size_t)qrows * h, kvrows, h, seed, layer_tid(l, K_K), 0, fan_scale(h),
+                         po::INIT_PLAIN, s);
+    po::launch_init_bf16(ly.wqkv + (size_t)(qrows + kvrows) * h, kvrows, h, seed, layer_tid(l, K_V), 0, fan_scale(h),
+                         po::INIT_PLAIN, s);
+    po::launch_init_bf16(ly.wo, h, ctxc, seed, layer_tid(l, K_O), 0, fan_scale(ctxc), po::INIT_PLAIN, s);
+    po::launch_init_bf16(ly.wgu, 2 * I, h, seed, layer_tid(l, K_GATE), layer_tid(l, K_UP), fan_scale(h),
+                         po::INIT_GATE_UP, s);
+    po::launch_init_bf16(ly.wdown, h, I, seed, layer_tid(l, K_DOWN), 0, fan_scale(I), po::INIT_PLAIN, s);
+    po::launch_init_norm(ly.attn_norm, h, seed, layer_tid(l, K_ATTN_NORM), s);
+    po::launch_init_norm(ly.mlp_norm, h, seed, layer_tid(l, K_MLP_NORM), s);
+    if (po::make_tmap_b(&ly.map_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b(&ly.map_o, ly.wo, ctxc, h, ctxc) ||
+        po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I))
+      return fail(PO_ERR_CUDA, "weight tensor-map encode failed");
+  }
+
+  // ---- activation arena (hybrid prefill: full-length hidden/qkv, chunk-bounded MLP intermediate)
+  const int xcols = h > ctxc ? h : ctxc;
+  const long long chunk_rows = c.chunk < T ? c.chunk : T;
+  if (dalloc(e, &e->resid, (size_t)T * h * 4, &e->arena_bytes) ||
+      dalloc(e, &e->xn, (size_t)T * xcols * 2, &e->arena_bytes) ||
+      dalloc(e, &e->qkv, (size_t)T * qkvc * 2, &e->arena_bytes) ||
+      dalloc(e, &e->act, (size_t)chunk_rows * I * 2, &e->arena_bytes) ||
+      dalloc(e, &e->rope, (size_t)T * (c.head_dim / 2) * sizeof(float2), &e->arena_bytes))
+    return fail(PO_ERR_CUDA, "arena allocation failed");
+  cudaMemsetAsync(e->qkv, 0, (size_t)T * qkvc * 2, s);
+  const long long max_blocks = T / c.block_tokens + 1;
+  if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
+      dalloc(e, &e->d_slots, (size_t)max_blocks * 4, &e->arena_bytes) ||
+      dalloc(e, &e->d_admit, (size_t)max_blocks * 8, &e->arena_bytes) ||
+      dalloc(e, &e->d_allowed, (size_t)c.vocab * 4, &e->arena_bytes) ||
+      dalloc(e, &e->d_logits, (size_t)c.vocab * 4, &e->arena_bytes) ||
+      dalloc(e, &e->d_probs, (size_t)c.vocab * 4, &e->arena_bytes) ||
+      dalloc(e, &e->d_argmax, 16, &e->arena_bytes))
+    return fail(PO_ERR_CUDA, "staging allocation failed");
+  if (halloc(&e->h_tokens, (size_t)T * 4) || halloc(&e->h_slots, (size_t)max_blocks * 4) ||
+      halloc(&e->h_admit, (size_t)max_blocks * 8) || halloc(&e->h_allowed, (size_t)c.vocab * 4) ||
+      halloc(&e->h_logits, (size_t)c.vocab * 4) || halloc(&e->h_probs, (size_t)c.vocab * 4) ||
+      halloc(&e->h_argmax, 16))
+    return fail(PO_ERR_CUDA, "pinned host allocation failed");
+  {
+    const std::vector<float> inv = rope_inv_freq(c);
+    const int half = c.head_dim / 2;
+    std::vector<float2> table((size_t)T * half);
+    for (long long p = 0; p < T; ++p)
+      for (int i = 0; i < half; ++i) {
+        const float ang = static_cast<float>(p) * inv[i];  // fp32 product, as in HF (inv_freq @ positions)
+        table[(size_t)p * half + i] = make_float2(static_cast<float>(std::cos(static_cast<double>(ang))),
+                                                  static_cast<float>(std::sin(static_cast<double>(ang))));
+      }
+    if (cudaMemcpyAsync(e->rope, table.data(), table.size() * sizeof(float2), cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+      return fail(PO_ERR_CUDA, "rope table upload failed");
+    cudaStreamSynchronize(s);
+  }
+  if (po::make_tmap_a(&e->map_xn, e->xn, h, T, h) || po::make_tmap_a(&e->map_ctx, e->xn, ctxc, T, ctxc) ||
+      po::make_tmap_a(&e->map_act, e->act, I, chunk_rows, I))
+    return fail(PO_ERR_CUDA, "activation tensor-map encode failed");
+
+  // ---- prefix pool: explicit size, or a profile run: what remains after weights + arena
+  if (cudaStreamSynchronize(s) != cudaSuccess) return fail(PO_ERR_CUDA, "init kernels failed");
+  const int64_t bb = e->block_bytes();
+  if (c.pool_blocks >= 0) {
+    e->pool_blocks = c.pool_blocks;
+  } else {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double frac = (c.pool_mem_fraction > 0 && c.pool_mem_fraction <= 1) ? c.pool_mem_fraction : 0.9;
+    const int64_t reserve = 2ll << 30;  // headroom for the CUDA context, cuBLAS/torch workspaces
+    const int64_t avail = (int64_t)free_b > reserve ? (int64_t)((free_b - reserve) * frac) : 0;
+    e->pool_blocks = avail / bb;
+  }
+  if (e->pool_blocks > 0 && dalloc(e, &e->pool, (size_t)(e->pool_blocks * bb), &e->pool_bytes))
+    return fail(PO_ERR_CUDA, "prefix pool allocation failed");
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  e->free_after = (int64_t)free_b;
+  *out = e;
+  return PO_OK;
+}
+
+int po_engine_info(po_engine* e, int64_t* out, int32_t n) {
+  if (!e || !out) return set_error(PO_ERR_ARG, "po_engine_info: null argument");
+  const int64_t v[7] = {e->pool_blocks, e->weight_bytes, e->arena_bytes, e->pool_bytes, e->block_bytes(),
+                        e->cfg.max_tokens, e->free_after};
+  for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
+  return PO_OK;
+}
+
+int po_last_service_ms(po_engine* e, float* ms) {
+  if (!e || !ms) return set_error(PO_ERR_ARG, "po_last_service_ms: null argument");
+  *ms = e->last_ms;
+  return PO_OK;
+}
+
+int po_pool_evict(po_engine* e, const int32_t* slots, int32_t n) {
+  if (!e) return set_error(PO_ERR_ARG, "po_pool_evict: null engine");
+  for (int i = 0; i < n; ++i)
+    if (slots[i] < 0 || slots[i] >= e->pool_blocks)
+      return set_error(PO_ERR_POOL, "po_pool_evict: slot %d out of range [0, %lld)", slots[i],
+                       (long long)e->pool_blocks);
+  return PO_OK;
+}
+
+int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, int64_t nelem) {
+  if (!e || !host) return set_error(PO_ERR_ARG, "po_load_weight: null argument");
+  const po_model_cfg& c = e->cfg;
+  const int h = c.hidden, I = c.intermediate;
+  const int qrows = c.n_heads * c.head_dim, kvrows = c.n_kv_heads * c.head_dim;
+  if (kind >= 1 && kind <= 9 && (layer < 0 || layer >= c.num_layers))
+    return set_error(PO_ERR_ARG, "po_load_weight: layer %d out of range", layer);
+  cudaSetDevice(e->device);
+  void* dst = nullptr;
+  int64_t expect = 0;
+  bool norm = false;
+  auto& ly = e->layers[(kind >= 1 && kind <= 9) ? layer : 0];
+  switch (kind) {
+    case 0: dst = e->embed; expect = (int64_t)c.vocab * h; break;
+    case 1: dst = ly.attn_norm; expect = h; norm = true; break;
+    case 2: dst = ly.wqkv; expect = (int64_t)qrows * h; break;
+    case 3: dst = ly.wqkv + (size_t)qrows * h; expect = (int64_t)kvrows * h; break;
+    case 4: dst = ly.wqkv + (size_t)(qrows + kvrows) * h; expect = (int64_t)kvrows * h; break;
+    case 5: dst = ly.wo; expect = (int64_t)h * qrows; break;
+    case 6: dst = ly.mlp_norm; expect = h; norm = true; break;
+    case 7:
+    case 8: expect = (int64_t)I * h; break;
+    case 9: dst = ly.wdown; expect = (int64_t)h * I; break;
+    case 10: dst = e->final_norm; expect = h; norm = true; break;
+    case 11: dst = e->lm_head; expect = (int64_t)c.vocab * h; break;
+    default: return set_error(PO_ERR_ARG, "po_load_weight: unknown kind %d", kind);
+  }
+  if (nelem != expect)
+    return set_error(PO_ERR_ARG, "po_load_weight: kind %d expects %lld elements, got %lld", kind, (long long)expect,
+                     (long long)nelem);
+  if (kind == 7 || kind == 8) {
+    // interleave into the fused gate/up layout: 16-row groups, gate first
+    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(host);
+    const int off = kind == 7 ? 0 : 16;
+    for (int g = 0; g < I / 16; ++g)
+      if (cudaMemcpy(ly.wgu + ((size_t)g * 32 + off) * h, src + (size_t)g * 16 * h, (size_t)16 * h * 2,
+                     cudaMemcpyHostToDevice) != cudaSuccess)
+        return set_error(PO_ERR_CUDA, "po_load_weight: copy failed");
+    return PO_OK;
+  }
+  if (cudaMemcpy(dst, host, (size_t)nelem * (norm ? 4 : 2), cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_error(PO_ERR_CUDA, "po_load_weight: copy failed");
+  return PO_OK;
+}
+
+int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
+               int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
+               float* out_probs, int32_t* out_argmax, void* stream) {
+  if (!e || !tokens || !allowed || n_allowed <= 0)
+    return set_error(PO_ERR_ARG, "po_prefill: null argument or empty allowed list");
+  const po_model_cfg& c = e->cfg;
+  if (n <= 0) return set_error(PO_ERR_ARG, "po_prefill: empty request");
+  if (n > c.max_tokens)
+    return set_error(PO_ERR_CAPACITY, "po_prefill: request of %d tokens exceeds MIL %d", n, c.max_tokens);
+  if (n_cached < 0 || n_cached > n || n_cached % c.block_tokens)
+    return set_error(PO_ERR_ARG, "po_prefill: need 0 <= n_cached <= n, block aligned (got %d of %d)", n_cached, n);
+  if (n_allowed > c.vocab) return set_error(PO_ERR_ARG, "po_prefill: more allowed ids than vocab rows");
+  const int bt = c.block_tokens;
+  if (n_blocks < 0 || n_blocks > n / bt) return set_error(PO_ERR_ARG, "po_prefill: n_blocks %d > n/bt", n_blocks);
+  if (n_cached / bt > n_blocks || (n_cached > 0 && !pool_block_ids))
+    return set_error(PO_ERR_ARG, "po_prefill: cached blocks need pool slots");
+  for (int i = 0; i < n_allowed; ++i)
+    if (allowed[i] < 0 || allowed[i] >= c.vocab)
+      return set_error(PO_ERR_ARG, "po_prefill: allowed id %d out of vocab", allowed[i]);
+  cudaSetDevice(e->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+
+  // a fully cached request still recomputes its last token to produce logits
+  const int n_c = n_cached < n ? n_cached : n - 1;
+  const int n_miss = n - n_c;
+  const int cached_blocks = (n_c + bt - 1) / bt;
+  int n_admit = 0;
+  for (int b = 0; b < n_blocks; ++b) {
+    const int slot = pool_block_ids[b];
+    if (b < n_cached / bt) {
+      if (slot < 0 || slot >= e->pool_blocks)
+        return set_error(PO_ERR_POOL, "po_prefill: cached block %d has invalid slot %d", b, slot);
+      if (b < cached_blocks) e->h_slots[b] = slot;
+    } else if (slot >= 0) {
+      if (slot >= e->pool_blocks) return set_error(PO_ERR_POOL, "po_prefill: admit slot %d out of range", slot);
+      e->h_admit[n_admit++] = make_int2(b, slot);
+    }
+  }
+  std::memcpy(e->h_tokens, tokens + n_c, (size_t)n_miss * 4);
+  std::memcpy(e->h_allowed, allowed, (size_t)n_allowed * 4);
+
+  const int h = c.hidden, I = c.intermediate, L = c.num_layers;
+  const int qkvc = e->qkv_cols(), ctxc = e->ctx_cols(), kvd = e->kv_dim();
+  const int kv_col0 = c.n_heads * c.head_dim;
+  cudaEventRecord(e->ev0, s);
+  cudaMemcpyAsync(e->d_tokens, e->h_tokens, (size_t)n_miss * 4, cudaMemcpyHostToDevice, s);
+  if (cached_blocks) cudaMemcpyAsync(e->d_slots, e->h_slots, (size_t)cached_blocks * 4, cudaMemcpyHostToDevice, s);
+  if (n_admit) cudaMemcpyAsync(e->d_admit, e->h_admit, (size_t)n_admit * 8, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(e->d_allowed, e->h_allowed, (size_t)n_allowed * 4, cudaMemcpyHostToDevice, s);
+
+  po::launch_embed(e->d_tokens, n_miss, e->embed, c.vocab, h, e->resid, s);
+  int rc = 0;
+  for (int l = 0; l < L && !rc; ++l) {
+    auto& ly = e->layers[l];
+    po::launch_rmsnorm(e->resid, n_miss, h, ly.attn_norm, c.rms_eps, e->xn, s);
+    po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
+    po::GemmArgs g{};
+    g.M = n_miss; g.N = qkvc; g.K = h;
+    g.out = e->qkv + (size_t)n_c * qkvc; g.ldo = qkvc;
+    g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
+    rc |= po::gemm_launch(e->map_xn, ly.map_qkv, po::EPI_QKV_ROPE, g, s);
+    po::launch_kv_scatter(e->qkv, qkvc, kv_col0, e->d_admit, n_admit, l, L, bt, kvd, e->pool, s);
+    rc |= po::attention_run(e->qkv, qkvc, n, n_c, c.n_heads, c.n_kv_heads, e->xn, ctxc, s);
+    po::GemmArgs go{};
+    go.M = n_miss; go.N = h; go.K = ctxc;
+    go.resid = e->resid; go.ldr = h;
+    rc |= po::gemm_launch(e->map_ctx, ly.map_o, po::EPI_RESID_F32, go, s);
+    for (int lo = 0; lo < n_miss && !rc; lo += c.chunk) {
+      const int rows = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
+      po::launch_rmsnorm(e->resid + (size_t)lo * h, rows, h, ly.mlp_norm, c.rms_eps, e->xn + (size_t)lo * h, s);
+      po::GemmArgs gu{};
+      gu.M = rows; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
+      gu.out = e->act; gu.ldo = I;
+      rc |= po::gemm_launch(e->map_xn, ly.map_gu, po::EPI_SILU_MUL, gu, s);
+      po::GemmArgs gd{};
+      gd.M = rows; gd.N = h; gd.K = I;
+      gd.resid = e->resid + (size_t)lo * h; gd.ldr = h;
+      rc |= po::gemm_launch(e->map_act, ly.map_down, po::EPI_RESID_F32, gd, s);
+    }
+  }
+  if (rc) return set_error(PO_ERR_CUDA, "po_prefill: kernel launch failed (%d): %s", rc,
+                           cudaGetErrorString(cudaGetLastError()));
+  po::launch_lm_head(e->resid + (size_t)(n_miss - 1) * h, h, e->final_norm, c.rms_eps, e->lm_head, e->d_allowed,
+                     n_allowed, e->d_logits, e->d_probs, e->d_argmax, s);
+  cudaMemcpyAsync(e->h_logits, e->d_logits, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(e->h_probs, e->d_probs, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(e->h_argmax, e->d_argmax, 4, cudaMemcpyDeviceToHost, s);
+  cudaEventRecord(e->ev1, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess)
+    return set_error(PO_ERR_CUDA, "po_prefill: forward failed: %s", cudaGetErrorString(cudaGetLastError()));
+  cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1);
+  if (out_logits) std::memcpy(out_logits, e->h_logits, (size_t)n_allowed * 4);
+  if (out_probs) std::memcpy(out_probs, e->h_probs, (size_t)n_allowed * 4);
+  if (out_argmax) *out_argmax = *e->h_argmax;
+  return PO_OK;
+}
+
+}  // extern "C"

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
-          tma_load_2d(sA + s * A_BYTES, &map_a, &full_bar[s], kb * BK, mb * BM);
+          tma_load_2d(sA + s * A_BYTES, &map_a, &full_bar[s], kb * BK, args.a_row0 + mb * BM);
           tma_load_2d(sB + s * B_BYTES, &map_b, &full_bar[s], kb * BK, nb * BN);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -272,6 +272,13 @@ int num_sms() {
   return n;
 }
 
+int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, int K) {
+  return make_tmap_2d_bf16(map, A, K, rows, lda * 2, BK, BM);
+}
+int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K) {
+  return make_tmap_2d_bf16(map, B, K, N, ldb * 2, BK, BN);
+}
+
 int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K) {
   if (M <= 0 || N % BN != 0 || K % BK != 0) return -3;
   plan->M = M;
@@ -283,7 +290,7 @@ int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long 
 }
 
 template <int EPI>
-static int launch(const GemmPlan& plan, const GemmArgs& args, cudaStream_t stream) {
+static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmArgs& args, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -291,8 +298,22 @@ static int launch(const GemmPlan& plan, const GemmArgs& args, cudaStream_t strea
   }
   const int tiles = ((args.M + BM - 1) / BM) * (args.N / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_kernel<EPI><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(plan.map_a, plan.map_b, args);
+  gemm_kernel<EPI><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(map_a, map_b, args);
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, const GemmArgs& args,
+                cudaStream_t stream) {
+  if (args.M <= 0) return 0;
+  if (args.N % BN || args.K % BK) return -3;
+  switch (epi) {
+    case EPI_BF16: return launch<EPI_BF16>(map_a, map_b, args, stream);
+    case EPI_RESID_F32: return launch<EPI_RESID_F32>(map_a, map_b, args, stream);
+    case EPI_SILU_MUL: return launch<EPI_SILU_MUL>(map_a, map_b, args, stream);
+    case EPI_QKV_ROPE: return launch<EPI_QKV_ROPE>(map_a, map_b, args, stream);
+    case EPI_F32: return launch<EPI_F32>(map_a, map_b, args, stream);
+    default: return -3;
+  }
 }
 
 int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t stream) {
@@ -300,14 +321,7 @@ int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t str
   args.M = plan.M;
   args.N = plan.N;
   args.K = plan.K;
-  switch (epi) {
-    case EPI_BF16: return launch<EPI_BF16>(plan, args, stream);
-    case EPI_RESID_F32: return launch<EPI_RESID_F32>(plan, args, stream);
-    case EPI_SILU_MUL: return launch<EPI_SILU_MUL>(plan, args, stream);
-    case EPI_QKV_ROPE: return launch<EPI_QKV_ROPE>(plan, args, stream);
-    case EPI_F32: return launch<EPI_F32>(plan, args, stream);
-    default: return -3;
-  }
+  return gemm_launch(plan.map_a, plan.map_b, epi, args, stream);
 }
 
 }  // namespace po

@@ -14,6 +14,7 @@ enum GemmEpi : int { EPI_BF16 = 0, EPI_RESID_F32 = 1, EPI_SILU_MUL = 2, EPI_QKV_
 
 struct GemmArgs {
   int M, N, K;
+  int a_row0;           // first row of A addressed through the A tensor map (chunked MLP)
   void* out;            // bf16 or fp32 output (EPI_BF16 / EPI_SILU_MUL / EPI_QKV_ROPE / EPI_F32)
   long long ldo;        // elements
   float* resid;         // EPI_RESID_F32
@@ -34,6 +35,11 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64
                       uint32_t box_inner, uint32_t box_outer);
 int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K);
 int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& args, cudaStream_t stream);
+// A/B maps built once (weights at init, activation buffers at init with their max rows).
+int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, const GemmArgs& args,
+                cudaStream_t stream);
+int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, int K);
+int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int num_sms();
 
 }  // namespace po
