@@ -218,9 +218,18 @@ def rope_table(cfg: Cfg, n: int) -> tuple[np.ndarray, np.ndarray]:
     return np.cos(a64).astype(np.float32), np.sin(a64).astype(np.float32)
 
 
-def rmsnorm(x: np.ndarray, gamma: np.ndarray, eps: float) -> np.ndarray:
+def rmsnorm(x: np.ndarray, gamma: np.ndarray, eps: float, rnd=None) -> np.ndarray:
     ms = np.mean(x * x, axis=-1, keepdims=True)
-    return bf16_round((x / np.sqrt(ms + eps)) * gamma).astype(np.float64)
+    y = (x / np.sqrt(ms + eps)) * gamma
+    return (rnd or _round64)(y)
+
+
+def _round64(x):
+    return bf16_round(x).astype(np.float64)
+
+
+def _exact(x):
+    return np.asarray(x, dtype=np.float64)
 
 
 def apply_rope(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
@@ -232,7 +241,8 @@ def apply_rope(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
     return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
 
 
-def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_hidden: bool = False):
+def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_hidden: bool = False,
+                  round_bf16: bool = True):
     """Prefill-only forward of one request; returns (logits, probs, argmax) over the allowed ids.
 
     Cached-prefix rows only serve as keys; their K/V equal what a cold forward computes (causality), so the
@@ -242,21 +252,26 @@ def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_
     n = len(toks)
     hd, hq, hkv = cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
     cos, sin = rope_table(cfg, n)
+    R = _round64 if round_bf16 else _exact
+    if not round_bf16:  # exact float64 Llama (for the transformers cross-check): exact RoPE angles too
+        inv = rope_inv_freq(cfg).astype(np.float64)
+        ang = np.arange(n, dtype=np.float64)[:, None] * inv[None, :]
+        cos, sin = np.cos(ang), np.sin(ang)
     x = w["embed"][toks.astype(np.int64)].astype(np.float64)
     for lw in w["layers"]:
-        xn = rmsnorm(x, lw["attn_norm"], cfg.rms_eps)
+        xn = rmsnorm(x, lw["attn_norm"], cfg.rms_eps, R)
         q = (xn @ lw["wq"].T.astype(np.float64)).reshape(n, hq, hd)
         k = (xn @ lw["wk"].T.astype(np.float64)).reshape(n, hkv, hd)
         v = (xn @ lw["wv"].T.astype(np.float64)).reshape(n, hkv, hd)
-        q = bf16_round(apply_rope(q, cos, sin)).astype(np.float64)
-        k = bf16_round(apply_rope(k, cos, sin)).astype(np.float64)
-        v = bf16_round(v).astype(np.float64)
-        ctx = bf16_round(causal_attention(q, k, v)).astype(np.float64).reshape(n, hq * hd)
+        q = R(apply_rope(q, cos, sin))
+        k = R(apply_rope(k, cos, sin))
+        v = R(v)
+        ctx = R(causal_attention(q, k, v)).reshape(n, hq * hd)
         x = x + ctx @ lw["wo"].T.astype(np.float64)
-        xn2 = rmsnorm(x, lw["mlp_norm"], cfg.rms_eps)
+        xn2 = rmsnorm(x, lw["mlp_norm"], cfg.rms_eps, R)
         x = x + gated_mlp(xn2, lw["w_gate"].T.astype(np.float64), lw["w_up"].T.astype(np.float64),
-                          lw["w_down"].T.astype(np.float64), round_act=True)
-    h_last = rmsnorm(x[-1:], w["final_norm"], cfg.rms_eps)[0]
+                          lw["w_down"].T.astype(np.float64), round_act=round_bf16)
+    h_last = rmsnorm(x[-1:], w["final_norm"], cfg.rms_eps, R)[0]
     alw = np.asarray(allowed, dtype=np.int64)
     logits = w["lm_head"][alw].astype(np.float64) @ h_last
     e = np.exp(logits - logits.max())

@@ -1,0 +1,363 @@
+"""Serving loop: router, per-GPU instances (queue + prefix pool + one request in flight), metrics.
+
+Contract of the reference engine loop (ps/sim.py:52-287), which a real engine must honour:
+  * Router: sticky user -> instance, first-seen round robin (ps/sim.py:52-66);
+  * one request in service per instance; n_cached probed when the request starts; its KV enters the
+    instance's prefix cache at completion; events at one timestamp run COMPLETE < FREE < ARRIVE (Q6);
+  * latency = completion - arrival, p99 by nearest rank (ps/sim.py:146-151, Q14).
+
+Two drivers share that logic:
+  simulate(...)  virtual clock; service time from a callable: the measured GPU forward of a live Engine
+                 (trace-driven, every request really runs) or a latency model (e.g. a JctProfile fitted on
+                 measured latencies). With the reference's analytic service time it reproduces sim.run
+                 record for record (tests/test_serving_parity.py).
+  Server         wall clock; one worker thread per engine, submit() -> Future[PrefillResult].
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+import threading
+import time
+from concurrent.futures import Future
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+from .cache import CacheConfig, PrefixCache, block_chain
+from .jct import JctProfile
+from .scheduling import (POLICY_SRJF, POLICY_SRJF_CALIBRATED, SCORING_PROFILE, Policy, SchedulingError,
+                         WaitingRequest, estimate_jct, schedule_next)
+
+EV_COMPLETE, EV_FREE, EV_ARRIVE = 0, 1, 2
+
+
+class ServingError(ValueError):
+    """Invalid serving configuration or trace."""
+
+
+@dataclass
+class Router:
+    """Sticky user -> instance assignment handed out round robin."""
+
+    num_instances: int
+    assignments: dict = field(default_factory=dict)
+    next_rr: int = 0
+
+    def route(self, request) -> int:
+        inst = self.assignments.get(request.user_id)
+        if inst is None:
+            inst = self.next_rr % self.num_instances
+            self.assignments[request.user_id] = inst
+            self.next_rr += 1
+        return inst
+
+
+@dataclass(frozen=True)
+class RequestRecord:
+    id: int
+    user_id: int
+    instance: int
+    arrival: float
+    start: float
+    completion: float
+    n_input: int
+    n_cached: int
+    token: int = -1  # allowed-token choice (real engine only)
+
+    @property
+    def latency(self) -> float:
+        return self.completion - self.arrival
+
+    @property
+    def service(self) -> float:
+        return self.completion - self.start
+
+
+def p99_nearest_rank(latencies) -> float:
+    if not latencies:
+        return 0.0
+    ordered = sorted(latencies)
+    return ordered[max(0, math.ceil(0.99 * len(ordered)) - 1)]
+
+
+@dataclass(frozen=True)
+class ServeReport:
+    records: tuple
+    mean_latency: float
+    p99_latency: float
+    throughput: float  # requests / s over the makespan
+    cache_hit_tokens: int
+    cache_hit_requests: int
+    per_instance_utilization: tuple
+    makespan: float
+    prompt_tokens_per_s: float  # all prompt tokens (n) / makespan
+    miss_tokens_per_s: float  # computed tokens (n - n_cached) / makespan
+
+    @property
+    def served(self) -> int:
+        return len(self.records)
+
+    @property
+    def utilization(self) -> float:
+        u = self.per_instance_utilization
+        return sum(u) / len(u) if u else 0.0
+
+
+def make_report(records: Sequence[RequestRecord], busy: Sequence[float], first_arrival: float) -> ServeReport:
+    if not records:
+        return ServeReport((), 0.0, 0.0, 0.0, 0, 0, tuple(0.0 for _ in busy), 0.0, 0.0, 0.0)
+    lat = [r.latency for r in records]
+    makespan = max(r.completion for r in records) - first_arrival
+    tp = len(records) / makespan if makespan > 0 else 0.0
+    toks = sum(r.n_input for r in records)
+    miss = sum(r.n_input - r.n_cached for r in records)
+    return ServeReport(
+        records=tuple(records), mean_latency=sum(lat) / len(lat), p99_latency=p99_nearest_rank(lat),
+        throughput=tp, cache_hit_tokens=sum(r.n_cached for r in records),
+        cache_hit_requests=sum(1 for r in records if r.n_cached > 0),
+        per_instance_utilization=tuple((b / makespan if makespan > 0 else 0.0) for b in busy), makespan=makespan,
+        prompt_tokens_per_s=toks / makespan if makespan > 0 else 0.0,
+        miss_tokens_per_s=miss / makespan if makespan > 0 else 0.0)
+
+
+@dataclass
+class Instance:
+    cache: PrefixCache
+    queue: list = field(default_factory=list)
+    busy: bool = False
+    busy_time: float = 0.0
+
+
+# service_fn(instance_index, waiting_request, n_cached, pool_block_ids) -> seconds, or (seconds, token)
+ServiceFn = Callable[[int, WaitingRequest, int, list], object]
+
+
+def simulate(trace, num_instances: int, policy: Policy, capacity_tokens: int, service_fn: ServiceFn,
+             block_tokens: int = 16, jct_profile: JctProfile | None = None, max_input: int | None = None
+             ) -> ServeReport:
+    """Virtual-clock serving run (the reference's event loop with a pluggable service time)."""
+    reqs = trace.requests
+    arr = [r.arrival for r in reqs]
+    if any(b < a for a, b in zip(arr, arr[1:])):
+        raise ServingError("trace arrivals must be nondecreasing")
+    if num_instances < 1:
+        raise ServingError("num_instances must be >= 1")
+    if max_input is not None:
+        over = [r.id for r in reqs if r.n_input > max_input]
+        if over:
+            from .engine import CapacityError
+            raise CapacityError(f"{len(over)} request(s) exceed MIL {max_input}: ids {over[:10]}")
+    needs_profile = policy.kind in (POLICY_SRJF, POLICY_SRJF_CALIBRATED) and policy.scoring == SCORING_PROFILE
+    if needs_profile and jct_profile is None:
+        raise SchedulingError("profile scoring requires a JctProfile")
+    if not reqs:
+        return make_report([], [0.0] * num_instances, 0.0)
+
+    insts = [Instance(PrefixCache(CacheConfig(capacity_tokens, block_tokens))) for _ in range(num_instances)]
+    router = Router(num_instances)
+    memo: dict = {}
+    events: list = []
+    seq = 0
+    for r in reqs:
+        heapq.heappush(events, (r.arrival, EV_ARRIVE, seq, r))
+        seq += 1
+    records: list = []
+
+    def start_next(idx: int, now: float):
+        nonlocal seq
+        inst = insts[idx]
+        wr = schedule_next(inst.queue, inst.cache, jct_profile, policy, now)
+        inst.queue.remove(wr)
+        n_cached = inst.cache.match_chain(wr.chain)
+        ncb = n_cached // block_tokens
+        slots = inst.cache.slots(wr.chain, ncb)
+        adm = inst.cache.begin_insert(wr.chain, now)
+        out = service_fn(idx, wr, n_cached, adm.pool_block_ids(ncb, slots))
+        service, token = (out if isinstance(out, tuple) else (out, -1))
+        inst.busy = True
+        inst.busy_time += service
+        heapq.heappush(events, (now + service, EV_FREE, seq, idx))
+        seq += 1
+        heapq.heappush(events, (now + service, EV_COMPLETE, seq, (idx, wr, n_cached, now, adm, token)))
+        seq += 1
+
+    while events:
+        now, kind, _, payload = heapq.heappop(events)
+        if kind == EV_ARRIVE:
+            r = payload
+            idx = router.route(r)
+            inst = insts[idx]
+            wr = WaitingRequest(request=r, arrival=now, chain=r.digest_chain(block_tokens, memo))
+            if policy.kind == POLICY_SRJF:
+                wr.frozen_jct = estimate_jct(r.n_input, inst.cache.match_chain(wr.chain, committed=True),
+                                             policy.scoring, jct_profile)
+            inst.queue.append(wr)
+            if not inst.busy:
+                start_next(idx, now)
+        elif kind == EV_FREE:
+            inst = insts[payload]
+            inst.busy = False
+            if inst.queue:
+                start_next(payload, now)
+        else:
+            idx, wr, n_cached, started, adm, token = payload
+            insts[idx].cache.commit(adm, now)
+            records.append(RequestRecord(wr.request.id, wr.request.user_id, idx, wr.arrival, started, now,
+                                         wr.request.n_input, n_cached, token))
+    assert len(records) == len(reqs), "conservation violated"
+    return make_report(records, [i.busy_time for i in insts], min(arr))
+
+
+def engine_service_fn(engines: Sequence, allowed: Sequence[int]) -> ServiceFn:
+    """Service function running the real forward on engines[instance]; returns (device seconds, token)."""
+
+    def fn(idx: int, wr: WaitingRequest, n_cached: int, pool_block_ids: list):
+        res = engines[idx].prefill(wr.request.tokens, allowed, n_cached, pool_block_ids)
+        return res.service_s, res.token
+
+    return fn
+
+
+def sweep_rates(trace, rates: Sequence[float], seed: int, run: Callable, keep_sessions: bool = True):
+    """Run `run(arrived_trace)` at each Poisson rate; returns [(rate, ServeReport)]."""
+    from .workload import poisson_arrivals
+
+    return [(q, run(poisson_arrivals(trace, q, seed=seed, keep_sessions=keep_sessions))) for q in rates]
+
+
+def qps_at_slo(results, slo_s: float) -> float:
+    """Largest swept rate whose p99 latency meets the SLO (0 if none)."""
+    ok = [q for q, rep in results if rep.p99_latency <= slo_s]
+    return max(ok) if ok else 0.0
+
+
+# ------------------------------------------------------------------ wall-clock server
+
+
+@dataclass
+class _Job:
+    wr: WaitingRequest
+    allowed: tuple
+    future: Future
+
+
+class _Worker(threading.Thread):
+    def __init__(self, server: "Server", idx: int, engine):
+        super().__init__(daemon=True, name=f"prefillonly-worker-{idx}")
+        self.server, self.idx, self.engine = server, idx, engine
+        self.inst = Instance(PrefixCache(CacheConfig(engine.capacity_tokens, engine.block_tokens)))
+        self.jobs: dict = {}
+        self.cv = threading.Condition()
+        self.stop = False
+
+    def enqueue(self, job: _Job, now: float):
+        with self.cv:
+            if self.server.policy.kind == POLICY_SRJF:
+                job.wr.frozen_jct = estimate_jct(job.wr.request.n_input,
+                                                 self.inst.cache.match_chain(job.wr.chain, committed=True),
+                                                 self.server.policy.scoring, self.server.jct_profile)
+            self.jobs[id(job.wr)] = job
+            self.inst.queue.append(job.wr)
+            self.cv.notify()
+
+    def run(self):
+        srv = self.server
+        eng = self.engine
+        bt = eng.block_tokens
+        while True:
+            with self.cv:
+                while not self.inst.queue and not self.stop:
+                    self.cv.wait()
+                if self.stop and not self.inst.queue:
+                    return
+                now = srv.clock()
+                wr = schedule_next(self.inst.queue, self.inst.cache, srv.jct_profile, srv.policy, now)
+                self.inst.queue.remove(wr)
+                job = self.jobs.pop(id(wr))
+                n_cached = self.inst.cache.match_chain(wr.chain)
+                ncb = n_cached // bt
+                slots = self.inst.cache.slots(wr.chain, ncb)
+                adm = self.inst.cache.begin_insert(wr.chain, now)
+            try:
+                res = eng.prefill(wr.request.tokens, job.allowed, n_cached, adm.pool_block_ids(ncb, slots))
+            except Exception as exc:  # the forward failed: its admitted blocks hold no K/V
+                with self.cv:
+                    self.inst.cache.abort(adm)
+                job.future.set_exception(exc)
+                continue
+            done = srv.clock()
+            with self.cv:
+                self.inst.cache.commit(adm, done)
+                self.inst.busy_time += done - now
+            rec = RequestRecord(wr.request.id, wr.request.user_id, self.idx, wr.arrival, now, done,
+                                wr.request.n_input, n_cached, res.token)
+            srv._record(rec)
+            job.future.set_result(res)
+
+
+class Server:
+    """Request-level data parallelism over engines (one per GPU), SRJF-calibrated by default."""
+
+    def __init__(self, engines: Sequence, policy: Policy | None = None, jct_profile: JctProfile | None = None):
+        if not engines:
+            raise ServingError("need at least one engine")
+        self.policy = policy or Policy.srjf_calibrated()
+        self.jct_profile = jct_profile
+        self.router = Router(len(engines))
+        self._t0 = time.monotonic()
+        self._lock = threading.Lock()
+        self.records: list = []
+        self._memo: dict = {}
+        self.workers = [_Worker(self, i, e) for i, e in enumerate(engines)]
+        for w in self.workers:
+            w.start()
+
+    def clock(self) -> float:
+        return time.monotonic() - self._t0
+
+    def reset_clock(self):
+        self._t0 = time.monotonic()
+
+    def _record(self, rec: RequestRecord):
+        with self._lock:
+            self.records.append(rec)
+
+    def submit(self, request, allowed: Sequence[int]) -> Future:
+        """Queue one request (duck type .id, .user_id, .n_input, .tokens); resolves to a PrefillResult."""
+        idx = self.router.route(request)
+        bt = self.workers[idx].engine.block_tokens
+        chain = request.digest_chain(bt, self._memo) if hasattr(request, "digest_chain") else \
+            block_chain(request.tokens, bt)
+        wr = WaitingRequest(request=request, arrival=self.clock(), chain=chain)
+        fut: Future = Future()
+        self.workers[idx].enqueue(_Job(wr, tuple(allowed), fut), wr.arrival)
+        return fut
+
+    def report(self) -> ServeReport:
+        with self._lock:
+            recs = sorted(self.records, key=lambda r: r.completion)
+        first = min((r.arrival for r in recs), default=0.0)
+        return make_report(recs, [w.inst.busy_time for w in self.workers], first)
+
+    def close(self):
+        for w in self.workers:
+            with w.cv:
+                w.stop = True
+                w.cv.notify()
+        for w in self.workers:
+            w.join()
+
+
+def replay(server: Server, trace, allowed: Sequence[int]) -> ServeReport:
+    """Inject the trace's arrivals in wall-clock time, wait for every completion, report."""
+    server.reset_clock()
+    futs = []
+    for r in trace.requests:
+        delay = r.arrival - server.clock()
+        if delay > 0:
+            time.sleep(delay)
+        futs.append(server.submit(r, allowed))
+    for f in futs:
+        f.result()
+    return server.report()
