@@ -100,6 +100,21 @@ int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached
                int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
                float* out_probs, int32_t* out_argmax, void* stream);
 
+/* Same forward on device-resident inputs (d_tokens: all n uint32 ids; d_allowed: n_allowed ids) with device
+ * outputs; asynchronous on `stream` (NULL = the engine's stream, see po_engine_stream). pool_block_ids is a
+ * host array as in po_prefill. Used to time the hot path with inputs already in HBM. */
+int po_prefill_device(po_engine* e, const uint32_t* d_tokens, int32_t n, int32_t n_cached, const int32_t* d_allowed,
+                      int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* d_logits,
+                      float* d_probs, int32_t* d_argmax, void* stream);
+int po_engine_stream(po_engine* e, void** stream);
+/* Kernel launches issued by the last forward. */
+int po_last_launches(po_engine* e, int32_t* n);
+/* Per-kernel-class CUDA-event timing over the forwards issued between begin and end. Classes: 0 embed,
+ * 1 rmsnorm, 2 kv_gather, 3 gemm_qkv_rope, 4 kv_scatter, 5 attention, 6 gemm_o_resid, 7 gemm_gate_up_silu,
+ * 8 gemm_down_resid, 9 lm_head. */
+int po_profile_begin(po_engine* e);
+int po_profile_end(po_engine* e, float* ms_per_class, int32_t* launches_per_class, int32_t n_classes);
+
 /* Device milliseconds of the last po_prefill (CUDA events around the forward on the engine stream). */
 int po_last_service_ms(po_engine* e, float* ms);
 

@@ -48,6 +48,11 @@ SIGNATURES = {
     "po_free": (_I32, [_VP]),
     "po_prefill": (_I32, [_VP, _VP, _I32, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "po_last_service_ms": (_I32, [_VP, _VP]),
+    "po_prefill_device": (_I32, [_VP, _VP, _I32, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
+    "po_engine_stream": (_I32, [_VP, _VP]),
+    "po_last_launches": (_I32, [_VP, _VP]),
+    "po_profile_begin": (_I32, [_VP]),
+    "po_profile_end": (_I32, [_VP, _VP, _VP, _I32]),
     "po_pool_evict": (_I32, [_VP, _VP, _I32]),
     "po_engine_info": (_I32, [_VP, _VP, _I32]),
     "po_load_weight": (_I32, [_VP, _I32, _I32, _VP, _I64]),

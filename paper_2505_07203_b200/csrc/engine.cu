@@ -72,6 +72,12 @@ struct po_engine {
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0;
   std::vector<void*> allocs;
   float last_ms = 0.f;
+  int last_launches = 0;
+  // per-kernel-class CUDA-event timing (bench roofline)
+  bool profiling = false;
+  int prof_used = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::vector<int> prof_class;
 
   int qkv_cols() const { return (cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim; }
   int kv_dim() const { return 2 * cfg.n_kv_heads * cfg.head_dim; }
@@ -151,6 +157,10 @@ int po_free(po_engine* e) {
   cudaFreeHost(e->h_logits);
   cudaFreeHost(e->h_probs);
   cudaFreeHost(e->h_argmax);
+  for (auto& pr : e->prof_events) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -349,31 +359,24 @@ int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, 
   return PO_OK;
 }
 
-int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
-               int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
-               float* out_probs, int32_t* out_argmax, void* stream) {
-  if (!e || !tokens || !allowed || n_allowed <= 0)
-    return set_error(PO_ERR_ARG, "po_prefill: null argument or empty allowed list");
+namespace {
+// Validate a request and stage its block table; returns n_c (computed-from prefix) or a negative status.
+int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, const int32_t* pool_block_ids,
+                  int32_t n_blocks, int* n_admit_out) {
   const po_model_cfg& c = e->cfg;
   if (n <= 0) return set_error(PO_ERR_ARG, "po_prefill: empty request");
   if (n > c.max_tokens)
     return set_error(PO_ERR_CAPACITY, "po_prefill: request of %d tokens exceeds MIL %d", n, c.max_tokens);
   if (n_cached < 0 || n_cached > n || n_cached % c.block_tokens)
     return set_error(PO_ERR_ARG, "po_prefill: need 0 <= n_cached <= n, block aligned (got %d of %d)", n_cached, n);
-  if (n_allowed > c.vocab) return set_error(PO_ERR_ARG, "po_prefill: more allowed ids than vocab rows");
+  if (n_allowed <= 0 || n_allowed > c.vocab)
+    return set_error(PO_ERR_ARG, "po_prefill: allowed list must hold 1..vocab ids (got %d)", n_allowed);
   const int bt = c.block_tokens;
   if (n_blocks < 0 || n_blocks > n / bt) return set_error(PO_ERR_ARG, "po_prefill: n_blocks %d > n/bt", n_blocks);
-  if (n_cached / bt > n_blocks || (n_cached > 0 && !pool_block_ids))
+  if (n_cached / bt > n_blocks || (n_blocks > 0 && !pool_block_ids))
     return set_error(PO_ERR_ARG, "po_prefill: cached blocks need pool slots");
-  for (int i = 0; i < n_allowed; ++i)
-    if (allowed[i] < 0 || allowed[i] >= c.vocab)
-      return set_error(PO_ERR_ARG, "po_prefill: allowed id %d out of vocab", allowed[i]);
-  cudaSetDevice(e->device);
-  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
-
   // a fully cached request still recomputes its last token to produce logits
   const int n_c = n_cached < n ? n_cached : n - 1;
-  const int n_miss = n - n_c;
   const int cached_blocks = (n_c + bt - 1) / bt;
   int n_admit = 0;
   for (int b = 0; b < n_blocks; ++b) {
@@ -387,52 +390,140 @@ int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached
       e->h_admit[n_admit++] = make_int2(b, slot);
     }
   }
-  std::memcpy(e->h_tokens, tokens + n_c, (size_t)n_miss * 4);
-  std::memcpy(e->h_allowed, allowed, (size_t)n_allowed * 4);
+  *n_admit_out = n_admit;
+  return n_c;
+}
 
+enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
+              KC_COUNT };
+
+// The hybrid-prefill forward on device-resident inputs; asynchronous on stream s.
+int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admit, const int* d_allowed,
+            int n_allowed, float* d_logits, float* d_probs, int* d_argmax, cudaStream_t s) {
+  const po_model_cfg& c = e->cfg;
+  const int bt = c.block_tokens;
+  const int n_miss = n - n_c;
+  const int cached_blocks = (n_c + bt - 1) / bt;
   const int h = c.hidden, I = c.intermediate, L = c.num_layers;
   const int qkvc = e->qkv_cols(), ctxc = e->ctx_cols(), kvd = e->kv_dim();
   const int kv_col0 = c.n_heads * c.head_dim;
-  cudaEventRecord(e->ev0, s);
-  cudaMemcpyAsync(e->d_tokens, e->h_tokens, (size_t)n_miss * 4, cudaMemcpyHostToDevice, s);
+  int launches = 0;
+  auto mark = [&](int cls, bool begin) {
+    if (!e->profiling) return;
+    if (begin) {
+      if (e->prof_used >= (int)e->prof_events.size()) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        e->prof_events.push_back({a, b});
+        e->prof_class.push_back(0);
+      }
+      e->prof_class[e->prof_used] = cls;
+      cudaEventRecord(e->prof_events[e->prof_used].first, s);
+    } else {
+      cudaEventRecord(e->prof_events[e->prof_used].second, s);
+      ++e->prof_used;
+    }
+  };
   if (cached_blocks) cudaMemcpyAsync(e->d_slots, e->h_slots, (size_t)cached_blocks * 4, cudaMemcpyHostToDevice, s);
   if (n_admit) cudaMemcpyAsync(e->d_admit, e->h_admit, (size_t)n_admit * 8, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(e->d_allowed, e->h_allowed, (size_t)n_allowed * 4, cudaMemcpyHostToDevice, s);
 
-  po::launch_embed(e->d_tokens, n_miss, e->embed, c.vocab, h, e->resid, s);
+  mark(KC_EMBED, true);
+  po::launch_embed(d_tok_miss, n_miss, e->embed, c.vocab, h, e->resid, s);
+  mark(KC_EMBED, false);
+  ++launches;
   int rc = 0;
   for (int l = 0; l < L && !rc; ++l) {
     auto& ly = e->layers[l];
+    mark(KC_NORM, true);
     po::launch_rmsnorm(e->resid, n_miss, h, ly.attn_norm, c.rms_eps, e->xn, s);
-    po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
+    mark(KC_NORM, false);
+    ++launches;
+    if (n_c > 0) {
+      mark(KC_GATHER, true);
+      po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
+      mark(KC_GATHER, false);
+      ++launches;
+    }
     po::GemmArgs g{};
     g.M = n_miss; g.N = qkvc; g.K = h;
     g.out = e->qkv + (size_t)n_c * qkvc; g.ldo = qkvc;
     g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
+    mark(KC_QKV, true);
     rc |= po::gemm_launch(e->map_xn, ly.map_qkv, po::EPI_QKV_ROPE, g, s);
-    po::launch_kv_scatter(e->qkv, qkvc, kv_col0, e->d_admit, n_admit, l, L, bt, kvd, e->pool, s);
+    mark(KC_QKV, false);
+    ++launches;
+    if (n_admit) {
+      mark(KC_SCATTER, true);
+      po::launch_kv_scatter(e->qkv, qkvc, kv_col0, e->d_admit, n_admit, l, L, bt, kvd, e->pool, s);
+      mark(KC_SCATTER, false);
+      ++launches;
+    }
+    mark(KC_ATTN, true);
     rc |= po::attention_run(e->qkv, qkvc, n, n_c, c.n_heads, c.n_kv_heads, e->xn, ctxc, s);
+    mark(KC_ATTN, false);
+    ++launches;
     po::GemmArgs go{};
     go.M = n_miss; go.N = h; go.K = ctxc;
     go.resid = e->resid; go.ldr = h;
+    mark(KC_O, true);
     rc |= po::gemm_launch(e->map_ctx, ly.map_o, po::EPI_RESID_F32, go, s);
+    mark(KC_O, false);
+    ++launches;
     for (int lo = 0; lo < n_miss && !rc; lo += c.chunk) {
       const int rows = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
+      mark(KC_NORM, true);
       po::launch_rmsnorm(e->resid + (size_t)lo * h, rows, h, ly.mlp_norm, c.rms_eps, e->xn + (size_t)lo * h, s);
+      mark(KC_NORM, false);
       po::GemmArgs gu{};
       gu.M = rows; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
       gu.out = e->act; gu.ldo = I;
+      mark(KC_GATE_UP, true);
       rc |= po::gemm_launch(e->map_xn, ly.map_gu, po::EPI_SILU_MUL, gu, s);
+      mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = rows; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h;
+      mark(KC_DOWN, true);
       rc |= po::gemm_launch(e->map_act, ly.map_down, po::EPI_RESID_F32, gd, s);
+      mark(KC_DOWN, false);
+      launches += 3;
     }
   }
   if (rc) return set_error(PO_ERR_CUDA, "po_prefill: kernel launch failed (%d): %s", rc,
                            cudaGetErrorString(cudaGetLastError()));
-  po::launch_lm_head(e->resid + (size_t)(n_miss - 1) * h, h, e->final_norm, c.rms_eps, e->lm_head, e->d_allowed,
-                     n_allowed, e->d_logits, e->d_probs, e->d_argmax, s);
+  mark(KC_LM_HEAD, true);
+  po::launch_lm_head(e->resid + (size_t)(n_miss - 1) * h, h, e->final_norm, c.rms_eps, e->lm_head, d_allowed,
+                     n_allowed, d_logits, d_probs, d_argmax, s);
+  mark(KC_LM_HEAD, false);
+  ++launches;
+  e->last_launches = launches;
+  if (cudaGetLastError() != cudaSuccess) return set_error(PO_ERR_CUDA, "po_prefill: launch error");
+  return PO_OK;
+}
+}  // namespace
+
+int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
+               int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
+               float* out_probs, int32_t* out_argmax, void* stream) {
+  if (!e || !tokens || !allowed) return set_error(PO_ERR_ARG, "po_prefill: null argument");
+  const po_model_cfg& c = e->cfg;
+  int n_admit = 0;
+  const int n_c = stage_request(e, n, n_cached, n_allowed, pool_block_ids, n_blocks, &n_admit);
+  if (n_c < 0) return n_c;
+  for (int i = 0; i < n_allowed; ++i)
+    if (allowed[i] < 0 || allowed[i] >= c.vocab)
+      return set_error(PO_ERR_ARG, "po_prefill: allowed id %d out of vocab", allowed[i]);
+  cudaSetDevice(e->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+  const int n_miss = n - n_c;
+  std::memcpy(e->h_tokens, tokens + n_c, (size_t)n_miss * 4);
+  std::memcpy(e->h_allowed, allowed, (size_t)n_allowed * 4);
+  cudaEventRecord(e->ev0, s);
+  cudaMemcpyAsync(e->d_tokens, e->h_tokens, (size_t)n_miss * 4, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(e->d_allowed, e->h_allowed, (size_t)n_allowed * 4, cudaMemcpyHostToDevice, s);
+  int rc = forward(e, e->d_tokens, n, n_c, n_admit, e->d_allowed, n_allowed, e->d_logits, e->d_probs, e->d_argmax, s);
+  if (rc) return rc;
   cudaMemcpyAsync(e->h_logits, e->d_logits, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(e->h_probs, e->d_probs, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(e->h_argmax, e->d_argmax, 4, cudaMemcpyDeviceToHost, s);
@@ -443,6 +534,61 @@ int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached
   if (out_logits) std::memcpy(out_logits, e->h_logits, (size_t)n_allowed * 4);
   if (out_probs) std::memcpy(out_probs, e->h_probs, (size_t)n_allowed * 4);
   if (out_argmax) *out_argmax = *e->h_argmax;
+  return PO_OK;
+}
+
+int po_prefill_device(po_engine* e, const uint32_t* d_tokens, int32_t n, int32_t n_cached, const int32_t* d_allowed,
+                      int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* d_logits,
+                      float* d_probs, int32_t* d_argmax, void* stream) {
+  if (!e || !d_tokens || !d_allowed || !d_logits || !d_probs || !d_argmax)
+    return set_error(PO_ERR_ARG, "po_prefill_device: null argument");
+  int n_admit = 0;
+  const int n_c = stage_request(e, n, n_cached, n_allowed, pool_block_ids, n_blocks, &n_admit);
+  if (n_c < 0) return n_c;
+  cudaSetDevice(e->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+  return forward(e, d_tokens + n_c, n, n_c, n_admit, d_allowed, n_allowed, d_logits, d_probs, d_argmax, s);
+}
+
+int po_engine_stream(po_engine* e, void** stream) {
+  if (!e || !stream) return set_error(PO_ERR_ARG, "po_engine_stream: null argument");
+  *stream = e->stream;
+  return PO_OK;
+}
+
+int po_last_launches(po_engine* e, int32_t* n) {
+  if (!e || !n) return set_error(PO_ERR_ARG, "po_last_launches: null argument");
+  *n = e->last_launches;
+  return PO_OK;
+}
+
+int po_profile_begin(po_engine* e) {
+  if (!e) return set_error(PO_ERR_ARG, "po_profile_begin: null engine");
+  e->profiling = true;
+  e->prof_used = 0;
+  return PO_OK;
+}
+
+int po_profile_end(po_engine* e, float* ms_per_class, int32_t* launches_per_class, int32_t n_classes) {
+  if (!e || !ms_per_class || !launches_per_class) return set_error(PO_ERR_ARG, "po_profile_end: null argument");
+  cudaSetDevice(e->device);
+  for (int i = 0; i < n_classes; ++i) {
+    ms_per_class[i] = 0.f;
+    launches_per_class[i] = 0;
+  }
+  for (int i = 0; i < e->prof_used; ++i) {
+    if (cudaEventSynchronize(e->prof_events[i].second) != cudaSuccess)
+      return set_error(PO_ERR_CUDA, "po_profile_end: event sync failed");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->prof_events[i].first, e->prof_events[i].second);
+    const int cls = e->prof_class[i];
+    if (cls < n_classes) {
+      ms_per_class[cls] += ms;
+      launches_per_class[cls] += 1;
+    }
+  }
+  e->profiling = false;
+  e->prof_used = 0;
   return PO_OK;
 }
 

@@ -131,6 +131,46 @@ class Engine:
         return PrefillResult(token=int(alw[idx]), index=idx, probs=probs, logits=logits, n_cached=int(n_cached),
                              service_s=float(ms.value) * 1e-3)
 
+    def prefill_device(self, d_tokens: int, n: int, d_allowed: int, n_allowed: int, d_logits: int, d_probs: int,
+                       d_argmax: int, n_cached: int = 0, pool_block_ids: Sequence[int] | None = None,
+                       stream: int | None = None):
+        """Asynchronous forward on device-resident inputs/outputs (raw device pointers)."""
+        ids = np.ascontiguousarray(pool_block_ids if pool_block_ids is not None else [], dtype=np.int32)
+        rc = _lib.load().po_prefill_device(self._h, d_tokens, n, int(n_cached), d_allowed, n_allowed,
+                                           ids.ctypes.data if len(ids) else None, len(ids), d_logits, d_probs,
+                                           d_argmax, stream)
+        try:
+            _lib.check(rc)
+        except _lib.PrefillOnlyError as err:
+            _raise(err)
+
+    @property
+    def stream(self) -> int:
+        """The engine's CUDA stream handle (cudaStream_t as int)."""
+        out = ctypes.c_void_p()
+        _lib.call("po_engine_stream", self._h, ctypes.addressof(out))
+        return int(out.value or 0)
+
+    @property
+    def last_launches(self) -> int:
+        out = ctypes.c_int32()
+        _lib.call("po_last_launches", self._h, ctypes.addressof(out))
+        return int(out.value)
+
+    KERNEL_CLASSES = ("embed", "rmsnorm", "kv_gather", "gemm_qkv_rope", "kv_scatter", "attention",
+                      "gemm_o_resid", "gemm_gate_up_silu", "gemm_down_resid", "lm_head")
+
+    def profile_begin(self):
+        _lib.call("po_profile_begin", self._h)
+
+    def profile_end(self) -> dict:
+        """{class: (milliseconds, launches)} accumulated since profile_begin (CUDA events, engine stream)."""
+        k = len(self.KERNEL_CLASSES)
+        ms = (ctypes.c_float * k)()
+        cnt = (ctypes.c_int32 * k)()
+        _lib.call("po_profile_end", self._h, ctypes.addressof(ms), ctypes.addressof(cnt), k)
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(self.KERNEL_CLASSES)}
+
     def load_weight(self, kind: int, layer: int, array: np.ndarray):
         """Overwrite one weight tensor (logical layout; see po_load_weight)."""
         arr = np.ascontiguousarray(array)
