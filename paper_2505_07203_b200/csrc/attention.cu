@@ -48,6 +48,87 @@ struct AttnArgs {
   float scale_log2;
 };
 
+// One 128-key tile of online softmax for this thread's query row (TMEM lane): reads S, writes P (bf16,
+// packed over the first 64 columns of S), keeps (m, l). `lim` = number of visible keys in the tile
+// (keys kbase + c with c < lim); only the MASKED instantiation tests it.
+template <bool MASKED>
+__device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, int lim, float sl2, int j, float& m,
+                                             float& l) {
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    uint32_t v0[32], v1[32];
+    tmem_ld32(s_addr + c * 32, v0);
+    tmem_ld32(s_addr + (c + 1) * 32, v1);
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float a0 = __uint_as_float(v0[e]), a1 = __uint_as_float(v0[e + 1]);
+      float b0 = __uint_as_float(v1[e]), b1 = __uint_as_float(v1[e + 1]);
+      if (MASKED) {
+        if (c * 32 + e >= lim) a0 = -INFINITY;
+        if (c * 32 + e + 1 >= lim) a1 = -INFINITY;
+        if ((c + 1) * 32 + e >= lim) b0 = -INFINITY;
+        if ((c + 1) * 32 + e + 1 >= lim) b1 = -INFINITY;
+      }
+      mx0 = fmaxf(mx0, fmaxf(a0, a1));
+      mx1 = fmaxf(mx1, fmaxf(b0, b1));
+    }
+  }
+  const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
+  const bool resc = m_new > m + RESCALE_THRESHOLD;
+  const float alpha = resc ? ex2_approx(m - m_new) : 1.0f;
+  if (j > 0 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[32];
+      tmem_ld32(o_addr + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+      tmem_st32(o_addr + c * 32, v);
+    }
+    tmem_st_wait();
+  }
+  if (resc) {
+    l *= alpha;
+    m = m_new;
+  }
+  const float nm = -m;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    uint32_t v0[32], v1[32];
+    tmem_ld32(s_addr + c * 32, v0);
+    tmem_ld32(s_addr + (c + 1) * 32, v1);
+    tmem_ld_wait();
+    uint32_t p0[16], p1[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      float x0 = ex2_approx(fmaf(__uint_as_float(v0[2 * e]), sl2, nm));
+      float x1 = ex2_approx(fmaf(__uint_as_float(v0[2 * e + 1]), sl2, nm));
+      float y0 = ex2_approx(fmaf(__uint_as_float(v1[2 * e]), sl2, nm));
+      float y1 = ex2_approx(fmaf(__uint_as_float(v1[2 * e + 1]), sl2, nm));
+      if (MASKED) {
+        if (c * 32 + 2 * e >= lim) x0 = 0.f;
+        if (c * 32 + 2 * e + 1 >= lim) x1 = 0.f;
+        if ((c + 1) * 32 + 2 * e >= lim) y0 = 0.f;
+        if ((c + 1) * 32 + 2 * e + 1 >= lim) y1 = 0.f;
+      }
+      s0 += x0;
+      s1 += x1;
+      s2 += y0;
+      s3 += y1;
+      p0[e] = pack_bf16(x0, x1);
+      p1[e] = pack_bf16(y0, y1);
+    }
+    // P columns [16c, 16c+32) lie inside S chunks already consumed (c/2 <= c)
+    tmem_st16(s_addr + c * 16, p0);
+    tmem_st16(s_addr + (c + 1) * 16, p1);
+  }
+  l += (s0 + s1) + (s2 + s3);
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map, const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -170,67 +251,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t s_addr = tmem + lane_base + i * 128;
     const uint32_t o_addr = tmem + lane_base + 256 + i * 128;
     const int pos = q_lo + r;
-    const float sl2 = a.scale_log2;
     float m = -INFINITY;  // running max (scaled, log2 units), possibly stale
     float l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&s_full[i], j & 1);
       tc_fence_after();
       const int kbase = j * BKV;
-      const bool need_mask = kbase + BKV - 1 > q_lo;
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_addr + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          float s = __uint_as_float(v[e]);
-          if (need_mask && kbase + c * 32 + e > pos) s = -INFINITY;
-          mx = fmaxf(mx, s);
-        }
+      // warp-uniform: only tiles crossing the diagonal of this query block pay for the mask
+      if (kbase + BKV - 1 > q_lo) {
+        softmax_tile<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l);
+      } else {
+        softmax_tile<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l);
       }
-      const float m_new = fmaxf(m, mx * sl2);
-      const bool resc = m_new > m + RESCALE_THRESHOLD;
-      const float alpha = resc ? ex2_approx(m - m_new) : 1.0f;
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t v[32];
-          tmem_ld32(o_addr + c * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-          tmem_st32(o_addr + c * 32, v);
-        }
-        tmem_st_wait();
-      }
-      if (resc) {
-        l *= alpha;
-        m = m_new;
-      }
-      float sum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_addr + c * 32, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float p0 = ex2_approx(fmaf(__uint_as_float(v[2 * e]), sl2, -m));
-          float p1 = ex2_approx(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m));
-          if (need_mask) {
-            if (kbase + c * 32 + 2 * e > pos) p0 = 0.f;
-            if (kbase + c * 32 + 2 * e + 1 > pos) p1 = 0.f;
-          }
-          sum += p0 + p1;
-          pk[e] = pack_bf16(p0, p1);
-        }
-        tmem_st16(s_addr + c * 16, pk);
-      }
-      l += sum;
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[i]);
