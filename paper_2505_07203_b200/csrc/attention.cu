@@ -46,6 +46,10 @@ struct AttnArgs {
   __nv_bfloat16* out;
   long long ldo;
   float scale_log2;
+  int splits;         // KV splits per (query block, head pair); 1 = write normalised bf16 output directly
+  int tiles_per_split;
+  float* part_o;      // [splits][n_q][hq*128] unnormalised fp32 partial outputs (splits > 1)
+  float2* part_ml;    // [splits][n_q][hq] (running max in log2 units, running sum)
 };
 
 // One 128-key tile of online softmax for this thread's query row (TMEM lane): reads S, writes P (bf16,
@@ -150,14 +154,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int lane = lane_id();
 
   // heaviest (longest causal extent) query blocks first
-  const int per_qb = a.hkv * a.pairs;
+  const int per_qb = a.hkv * a.pairs * a.splits;
   const int qb = a.num_qb - 1 - blockIdx.x / per_qb;
-  const int rem = blockIdx.x % per_qb;
+  int rem = blockIdx.x % per_qb;
+  const int split = rem % a.splits;
+  rem /= a.splits;
   const int g = rem / a.pairs;
   const int h0 = g * (2 * a.pairs) + 2 * (rem % a.pairs);
   const int q_lo = a.q_offset + qb * BQ;                    // position of query row 0 of this block
   const int q_hi = min(q_lo + BQ - 1, a.n_total - 1);       // last real query position
-  const int n_tiles = q_hi / BKV + 1;
+  const int all_tiles = q_hi / BKV + 1;
+  const int t0 = split * a.tiles_per_split;                 // this CTA's KV tile range [t0, t0 + n_tiles)
+  const int n_tiles = max(0, min(all_tiles, t0 + a.tiles_per_split) - t0);
+
+  if (n_tiles == 0) return;  // a KV split past this query block's causal extent (uniform across the CTA)
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&map);
@@ -186,11 +196,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
-        tma_load_2d_hint(sK + st * TILE_BYTES, &map, &k_full[st], kcol, j * BKV, keep);
-        tma_load_2d_hint(sK + st * TILE_BYTES + BOX_BYTES, &map, &k_full[st], kcol + 64, j * BKV, keep);
+        const int kr = (t0 + j) * BKV;
+        tma_load_2d_hint(sK + st * TILE_BYTES, &map, &k_full[st], kcol, kr, keep);
+        tma_load_2d_hint(sK + st * TILE_BYTES + BOX_BYTES, &map, &k_full[st], kcol + 64, kr, keep);
         mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
-        tma_load_2d_hint(sV + st * TILE_BYTES, &map, &v_full[st], vcol, j * BKV, keep);
-        tma_load_2d_hint(sV + st * TILE_BYTES + BOX_BYTES, &map, &v_full[st], vcol + 64, j * BKV, keep);
+        tma_load_2d_hint(sV + st * TILE_BYTES, &map, &v_full[st], vcol, kr, keep);
+        tma_load_2d_hint(sV + st * TILE_BYTES + BOX_BYTES, &map, &v_full[st], vcol + 64, kr, keep);
       }
     }
     __syncwarp();
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&s_full[i], j & 1);
       tc_fence_after();
-      const int kbase = j * BKV;
+      const int kbase = (t0 + j) * BKV;
       // warp-uniform: only tiles crossing the diagonal of this query block pay for the mask
       if (kbase + BKV - 1 > q_lo) {
         softmax_tile<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l);
@@ -269,24 +280,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     mbar_wait(&o_final[i], 0);
     tc_fence_after();
-    const float inv = 1.0f / l;
     const int row = qb * BQ + r;
-    __nv_bfloat16* dst = a.out + (long long)row * a.ldo + (h0 + i) * HD;
+    if (a.splits == 1) {
+      const float inv = 1.0f / l;
+      __nv_bfloat16* dst = a.out + (long long)row * a.ldo + (h0 + i) * HD;
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld32(o_addr + c * 32, v);
-      tmem_ld_wait();
-      if (row < a.n_q) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(o_addr + c * 32, v);
+        tmem_ld_wait();
+        if (row < a.n_q) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          d4[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv),
-                             pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
-                             pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv),
-                             pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv));
+          for (int q = 0; q < 4; ++q) {
+            d4[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv),
+                               pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
+                               pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv),
+                               pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv));
+          }
         }
       }
+    } else {
+      // split-KV partial: unnormalised O, running max m (log2 units) and sum l for the combine kernel
+      const long long prow = (long long)split * a.n_q + row;
+      float4* dst = reinterpret_cast<float4*>(a.part_o + prow * (a.hq * HD) + (h0 + i) * HD);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(o_addr + c * 32, v);
+        tmem_ld_wait();
+        if (row < a.n_q) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[c * 8 + q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        }
+      }
+      if (row < a.n_q) a.part_ml[prow * a.hq + h0 + i] = make_float2(m, l);
     }
   }
 
@@ -298,21 +328,78 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-struct AttnPlan {
-  CUtensorMap map;
-};
+// out[row, h, :] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s over the KV splits that exist for the row's block
+__global__ void attn_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml, int n_q,
+                                    int hq, int splits, int tiles_per_split, int q_offset, int n_total,
+                                    __nv_bfloat16* __restrict__ out, long long ldo) {
+  const long long total = (long long)n_q * hq * (HD / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q4 = static_cast<int>(i % (HD / 4));
+    const long long rh = i / (HD / 4);
+    const int h = static_cast<int>(rh % hq);
+    const int row = static_cast<int>(rh / hq);
+    const int qb = row / BQ;
+    const int q_hi = min(q_offset + qb * BQ + BQ - 1, n_total - 1);
+    const int all_tiles = q_hi / BKV + 1;
+    const int ns = min(splits, (all_tiles + tiles_per_split - 1) / tiles_per_split);
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[((long long)s * n_q + row) * hq + h].x);
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < ns; ++s) {
+      const float2 ml = part_ml[((long long)s * n_q + row) * hq + h];
+      const float w = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+      L += w * ml.y;
+      const float4 o = reinterpret_cast<const float4*>(part_o + ((long long)s * n_q + row) * hq * HD + h * HD)[q4];
+      acc.x += w * o.x;
+      acc.y += w * o.y;
+      acc.z += w * o.z;
+      acc.w += w * o.w;
+    }
+    const float inv = 1.0f / L;
+    reinterpret_cast<uint2*>(out + (long long)row * ldo + h * HD)[q4] =
+        make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+  }
+}
+
+// KV splits for a launch: split only when the (query block x head pair) grid cannot fill the SMs.
+void attention_split_plan(int n_total, int q_offset, int hq, int hkv, int* splits, int* tiles_per_split) {
+  const int n_q = n_total - q_offset;
+  const int num_qb = (n_q + BQ - 1) / BQ;
+  const int base = num_qb * hkv * (hq / hkv / 2);
+  const int max_tiles = (n_total - 1) / BKV + 1;
+  int s = 1;
+  if (base < 148 && max_tiles >= 8) {
+    s = (2 * 148 + base - 1) / base;
+    s = min(s, max_tiles / 4);
+    s = min(s, 32);
+    s = max(s, 1);
+  }
+  const int tps = (max_tiles + s - 1) / s;
+  *tiles_per_split = tps;
+  *splits = (max_tiles + tps - 1) / tps;
+}
+
+size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv) {
+  int s, tps;
+  attention_split_plan(n_total, q_offset, hq, hkv, &s, &tps);
+  if (s == 1) return 0;
+  const size_t n_q = n_total - q_offset;
+  return (size_t)s * n_q * hq * (HD * sizeof(float) + sizeof(float2));
+}
 
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, void* workspace, size_t workspace_bytes) {
   if (hq % hkv || (hq / hkv) % 2) return -3;
-  AttnPlan plan;
-  if (make_tmap_2d_bf16(&plan.map, qkv, ld, n_total, ld * 2, 64, 128)) return -2;
+  CUtensorMap map;
+  if (make_tmap_2d_bf16(&map, qkv, ld, n_total, ld * 2, 64, 128)) return -2;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     configured = true;
   }
-  AttnArgs a;
+  AttnArgs a{};
   a.n_total = n_total;
   a.q_offset = q_offset;
   a.n_q = n_total - q_offset;
@@ -323,8 +410,25 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
   a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
-  const int grid = a.num_qb * hkv * a.pairs;
-  attn_fwd_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(plan.map, a);
+  attention_split_plan(n_total, q_offset, hq, hkv, &a.splits, &a.tiles_per_split);
+  const size_t need = attention_workspace_bytes(n_total, q_offset, hq, hkv);
+  if (a.splits > 1 && (!workspace || workspace_bytes < need)) {
+    a.splits = 1;  // no workspace: fall back to the unsplit kernel (same kernel, full KV range per CTA)
+    a.tiles_per_split = (n_total - 1) / BKV + 1;
+  }
+  if (a.splits > 1) {
+    a.part_o = static_cast<float*>(workspace);
+    a.part_ml = reinterpret_cast<float2*>(static_cast<char*>(workspace) +
+                                          (size_t)a.splits * a.n_q * hq * HD * sizeof(float));
+  }
+  const int grid = a.num_qb * hkv * a.pairs * a.splits;
+  attn_fwd_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(map, a);
+  if (a.splits > 1) {
+    const long long total = (long long)a.n_q * hq * (HD / 4);
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+    attn_combine_kernel<<<blocks, 256, 0, stream>>>(a.part_o, a.part_ml, a.n_q, hq, a.splits, a.tiles_per_split,
+                                                    q_offset, n_total, a.out, ldo);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
@@ -339,8 +443,13 @@ extern "C" int po_op_attention(const void* qkv, int64_t ld, int32_t n_total, int
     return po::set_error(PO_ERR_ARG, "po_op_attention: heads %d/%d must give an even GQA group", n_heads, n_kv_heads);
   if (ld < (int64_t)(n_heads + 2 * n_kv_heads) * 128 || ld % 8)
     return po::set_error(PO_ERR_ARG, "po_op_attention: ld %lld too small or unaligned", (long long)ld);
-  int rc = po::attention_run(qkv, ld, n_total, q_offset, n_heads, n_kv_heads, out, ldo,
-                             static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t ws_bytes = po::attention_workspace_bytes(n_total, q_offset, n_heads, n_kv_heads);
+  void* ws = nullptr;
+  if (ws_bytes && cudaMallocAsync(&ws, ws_bytes, st) != cudaSuccess)
+    return po::set_error(PO_ERR_CUDA, "po_op_attention: workspace allocation failed");
+  int rc = po::attention_run(qkv, ld, n_total, q_offset, n_heads, n_kv_heads, out, ldo, st, ws, ws_bytes);
+  if (ws) cudaFreeAsync(ws, st);
   if (rc) return po::set_error(PO_ERR_CUDA, "po_op_attention: failed (%d): %s", rc,
                                cudaGetErrorString(cudaGetLastError()));
   return PO_OK;

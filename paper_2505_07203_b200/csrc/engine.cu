@@ -19,12 +19,14 @@
 #include "kernels.cuh"
 #include <cmath>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 namespace po {
 int set_error(int code, const char* fmt, ...);
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
-                  cudaStream_t stream);
+                  cudaStream_t stream, void* workspace, size_t workspace_bytes);
+size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv);
 }  // namespace po
 
 struct po_engine {
@@ -49,6 +51,8 @@ struct po_engine {
   __nv_bfloat16* qkv = nullptr;
   __nv_bfloat16* act = nullptr;
   float2* rope = nullptr;
+  void* attn_ws = nullptr;  // split-KV partials for short-query (prefix-hit) requests
+  size_t attn_ws_bytes = 0;
   CUtensorMap map_xn, map_ctx, map_act;
   // per-request device staging
   uint32_t* d_tokens = nullptr;
@@ -236,6 +240,14 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       dalloc(e, &e->rope, (size_t)T * (c.head_dim / 2) * sizeof(float2), &e->arena_bytes))
     return fail(PO_ERR_CUDA, "arena allocation failed");
   cudaMemsetAsync(e->qkv, 0, (size_t)T * qkvc * 2, s);
+  {
+    // split-KV workspace: largest need over query lengths that trigger splitting, at n_total = max_tokens
+    size_t ws = 0;
+    for (int nq = 1; nq <= 148 * 128 && nq <= T; nq += 64)
+      ws = std::max(ws, po::attention_workspace_bytes((int)T, (int)T - nq, c.n_heads, c.n_kv_heads));
+    e->attn_ws_bytes = ws;
+    if (ws && dalloc(e, &e->attn_ws, ws, &e->arena_bytes)) return fail(PO_ERR_CUDA, "attention workspace failed");
+  }
   const long long max_blocks = T / c.block_tokens + 1;
   if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_slots, (size_t)max_blocks * 4, &e->arena_bytes) ||
@@ -460,7 +472,8 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       ++launches;
     }
     mark(KC_ATTN, true);
-    rc |= po::attention_run(e->qkv, qkvc, n, n_c, c.n_heads, c.n_kv_heads, e->xn, ctxc, s);
+    rc |= po::attention_run(e->qkv, qkvc, n, n_c, c.n_heads, c.n_kv_heads, e->xn, ctxc, s, e->attn_ws,
+                            e->attn_ws_bytes);
     mark(KC_ATTN, false);
     ++launches;
     po::GemmArgs go{};

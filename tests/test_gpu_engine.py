@@ -95,24 +95,36 @@ def test_chunk_size_does_not_change_result():
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
-def test_prefix_pool_reuse_is_bit_exact(tiny_engine):
+def test_prefix_pool_reuse_matches_oracle(tiny_engine):
+    """K/V served from the prefix pool (cached rows only act as keys) gives the oracle's answer.
+
+    Short-query requests run split-KV attention (different summation order than the cold forward), so
+    warm and cold forwards agree within the stated tolerance rather than bit for bit.
+    """
     bt = 16
     base = tokens_for(11, 1024)
-    # request A: cold, admit all 64 blocks into slots 100..163
-    slots_a = list(range(100, 164))
+    slots_a = list(range(100, 164))  # request A: cold, admit all 64 blocks into slots 100..163
     tiny_engine.prefill(base, YES_NO, n_cached=0, pool_block_ids=slots_a)
-    # request B shares A's first 640 tokens, then diverges
-    b = np.concatenate([base[:640], tokens_for(12, 500)])
-    cold = tiny_engine.prefill(b, YES_NO)
+    b = np.concatenate([base[:640], tokens_for(12, 500)])  # request B shares A's first 640 tokens
     n_cached = 640
     ids = slots_a[: n_cached // bt] + [-1] * (len(b) // bt - n_cached // bt)
     warm = tiny_engine.prefill(b, YES_NO, n_cached=n_cached, pool_block_ids=ids)
-    assert np.array_equal(cold.logits, warm.logits)
     assert warm.n_cached == 640
-    # fully cached request: recompute only the last token
+    check_against_oracle(TINY, warm, b, YES_NO, 42)
+    cold = tiny_engine.prefill(b, YES_NO)
+    assert np.abs(warm.logits - cold.logits).max() <= LOGIT_ATOL
+    # fully cached request (SURVEY H7): only the last token is recomputed
     full = tiny_engine.prefill(base, YES_NO, n_cached=1024, pool_block_ids=slots_a)
-    cold_a = tiny_engine.prefill(base, YES_NO)
-    assert np.array_equal(full.logits, cold_a.logits)
+    check_against_oracle(TINY, full, base, YES_NO, 42)
+
+
+def test_admission_writes_pool_then_long_hit(tiny_engine):
+    """Blocks admitted by one request serve a later request whose miss part is long (unsplit attention)."""
+    base = tokens_for(21, 3000)
+    slots = list(range(200, 200 + 3000 // 16))
+    tiny_engine.prefill(base[:2048], YES_NO, 0, slots[:128])
+    res = tiny_engine.prefill(base, YES_NO, 2048, slots[:128] + [-1] * (3000 // 16 - 128))
+    check_against_oracle(TINY, res, base, YES_NO, 42)
 
 
 def test_capacity_error(tiny_engine):
