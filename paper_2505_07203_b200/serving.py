@@ -219,6 +219,32 @@ def engine_service_fn(engines: Sequence, allowed: Sequence[int]) -> ServiceFn:
     return fn
 
 
+def shard_trace(trace, rank: int, world: int):
+    """Requests the sticky router sends to instance `rank` (request-level DP: each GPU serves its own users).
+
+    Routing depends only on first-arrival order of users, so every rank computes the same assignment locally;
+    no collective is needed on the data path.
+    """
+    router = Router(world)
+    mine = tuple(r for r in trace.requests if router.route(r) == rank)
+    return type(trace)(trace.name, trace.seed, mine)
+
+
+def merge_records(per_rank: Sequence[Sequence[RequestRecord]], world: int) -> ServeReport:
+    """Global report from per-rank records (rank r's records carry instance 0 locally -> r)."""
+    recs, busy = [], []
+    for rank, rr in enumerate(per_rank):
+        b = 0.0
+        for r in rr:
+            recs.append(RequestRecord(r.id, r.user_id, rank, r.arrival, r.start, r.completion, r.n_input,
+                                      r.n_cached, r.token))
+            b += r.service
+        busy.append(b)
+    recs.sort(key=lambda r: (r.completion, r.id))
+    first = min((r.arrival for r in recs), default=0.0)
+    return make_report(recs, busy, first)
+
+
 def sweep_rates(trace, rates: Sequence[float], seed: int, run: Callable, keep_sessions: bool = True):
     """Run `run(arrived_trace)` at each Poisson rate; returns [(rate, ServeReport)]."""
     from .workload import poisson_arrivals

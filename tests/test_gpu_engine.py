@@ -119,7 +119,7 @@ def test_prefix_pool_reuse_matches_oracle(tiny_engine):
 
 
 def test_admission_writes_pool_then_long_hit(tiny_engine):
-    """Blocks admitted by one request serve a later request whose miss part is long (unsplit attention)."""
+    """Blocks admitted by one request (K/V written during its forward) serve a later, longer request."""
     base = tokens_for(21, 3000)
     slots = list(range(200, 200 + 3000 // 16))
     tiny_engine.prefill(base[:2048], YES_NO, 0, slots[:128])
