@@ -202,13 +202,18 @@ def workload_config(args, world) -> dict:
 
 
 # ---------------------------------------------------------------------------------------------- GPU arm
-def gemm_flops_per_class(M, n_miss: int) -> dict:
+def executed_flops_per_class(M, n: int, last_row_only: bool) -> dict:
+    """Executed FLOPs per kernel class for one cold n-token request (the last layer runs attention, O and
+    the MLP for the final row only when last_row_only)."""
     h, I = M.hidden, M.intermediate
     qkvc = (M.n_heads + 2 * M.n_kv_heads) * M.head_dim
     ctx = M.n_heads * M.head_dim
     L = M.num_layers
-    return {"gemm_qkv_rope": 2.0 * n_miss * h * qkvc * L, "gemm_o_resid": 2.0 * n_miss * ctx * h * L,
-            "gemm_gate_up_silu": 2.0 * n_miss * h * 2 * I * L, "gemm_down_resid": 2.0 * n_miss * I * h * L}
+    rows = (L - 1) * n + 1 if last_row_only else L * n  # row-layers through attention output / O / MLP
+    pairs = (L - 1) * n * n / 2.0 + n if last_row_only else L * n * n / 2.0
+    return {"gemm_qkv_rope": 2.0 * n * h * qkvc * L, "gemm_o_resid": 2.0 * rows * ctx * h,
+            "gemm_gate_up_silu": 2.0 * rows * h * 2 * I, "gemm_down_resid": 2.0 * rows * I * h,
+            "attention": 4.0 * h * pairs}
 
 
 def main():
@@ -308,8 +313,7 @@ def main():
     # ---------------- roofline per kernel class (algorithmic FLOPs / CUDA-event time in the timed region)
     peaks, peak_src = load_peaks()
     sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    cls_flops = gemm_flops_per_class(M, n)
-    cls_flops["attention"] = M.attn_flops_per_pair() * (n * n) / 2.0
+    cls_flops = executed_flops_per_class(M, n, eng.last_row_only)
     total_ms = sum(v[0] for v in prof.values())
     traffic = {}
     tpath = ROOT / "profiles" / "ncu_traffic.json"
@@ -330,10 +334,18 @@ def main():
                 "peak_source": f"{peak_src}: bf16_tflops_sustained (kernel timed inside a long step); "
                                f"burst {peaks['bf16_tflops']} gives frac {t['frac_of_burst']:.3f}",
                 "per_launch": f"{cls_flops[top] / max(1, prof[top][1] // K):.4g} algorithmic FLOP per launch"}
+    from paper_2505_07203_b200.config import executed_flops
+
     whole = M.request_flops(n) * world * K / (elapsed_ms / 1e3) / 1e12
+    exe = executed_flops(M, n, 0, eng.last_row_only)
+    whole_exe = exe * world * K / (elapsed_ms / 1e3) / 1e12
     step_roofline = {"achieved": whole, "unit": "TFLOP/s", "frac": whole / world / sustained,
                      "frac_of_burst": whole / world / peaks["bf16_tflops"],
-                     "flops_per_request": M.request_flops(n)}
+                     "flops_per_request": M.request_flops(n),
+                     "executed_flops_per_request": exe, "achieved_executed": whole_exe,
+                     "frac_executed": whole_exe / world / sustained,
+                     "note": "algorithmic = reference accounting (ps/costs.py:126-136,275-277); executed skips the "
+                             "last layer's attention/O/MLP for rows other than the final one (exact)"}
 
     # ---------------- QPS at P99 SLO (calibrated SRJF + prefix pool, DP over all ranks)
     qps = None

@@ -81,6 +81,8 @@ typedef struct po_model_cfg {
   int32_t block_tokens;      /* prefix-pool block (CacheConfig.block_tokens = 16, ps/cache.py:65-80)   */
   int64_t pool_blocks;       /* prefix-pool capacity in blocks; < 0 = size by a profile run            */
   double pool_mem_fraction;  /* profile run: fraction of HBM left after the arena given to the pool    */
+  int32_t last_row_only;     /* 1: in the last layer run attention/O/MLP for the final row only (exact:    */
+                             /*    only that row reaches the LM head); 0: every row through every layer  */
 } po_model_cfg;
 
 typedef struct po_engine po_engine;

@@ -108,15 +108,32 @@ class PoModelCfg(ctypes.Structure):
         ("block_tokens", ctypes.c_int32),
         ("pool_blocks", ctypes.c_int64),
         ("pool_mem_fraction", ctypes.c_double),
+        ("last_row_only", ctypes.c_int32),
     ]
 
 
 def to_c_cfg(model: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK, block_tokens: int = BLOCK_TOKENS,
-             pool_blocks: int = -1, pool_mem_fraction: float = 0.9) -> PoModelCfg:
+             pool_blocks: int = -1, pool_mem_fraction: float = 0.9, last_row_only: bool = True) -> PoModelCfg:
     d = asdict(model)
     d.pop("name")
     return PoModelCfg(**d, max_tokens=max_tokens, chunk=chunk, block_tokens=block_tokens, pool_blocks=pool_blocks,
-                      pool_mem_fraction=pool_mem_fraction)
+                      pool_mem_fraction=pool_mem_fraction, last_row_only=int(last_row_only))
+
+
+def executed_flops(model: ModelConfig, n: int, n_cached: int = 0, last_row_only: bool = True) -> float:
+    """FLOPs the engine actually executes: with last_row_only the last layer runs attention, O-proj and the
+    MLP for the final row only (its K/V are still computed for every row)."""
+    full = model.request_flops(n, n_cached)
+    if not last_row_only:
+        return full
+    h, i_ = model.hidden, model.intermediate
+    L = model.num_layers
+    miss = n - n_cached
+    rows_skipped = max(0, miss - 1)
+    o_mlp_per_row = 2.0 * h * (model.n_heads * model.head_dim) + 6.0 * h * i_
+    attn_layer = model.attn_flops_per_pair() / L * (n * n - n_cached * n_cached) / 2.0
+    attn_last_row = model.attn_flops_per_pair() / L * n
+    return full - rows_skipped * o_mlp_per_row - (attn_layer - attn_last_row)
 
 
 __all__ = ["ModelConfig", "PoModelCfg", "to_c_cfg", "get_preset", "PRESETS", "TINY", "LLAMA_3_1_8B",

@@ -42,7 +42,12 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
   args.rope = static_cast<const float2*>(rope_table);
   args.pos_offset = pos_offset;
   args.rope_cols = rope_cols;
-  rc = po::gemm_run(plan, epi, args, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t ws = po::gemm_split_ws_bytes(M, N, K);
+  if (ws && cudaMallocAsync(reinterpret_cast<void**>(&args.split_ws), ws, st) != cudaSuccess)
+    return po::set_error(PO_ERR_CUDA, "po_op_gemm: split-K workspace allocation failed");
+  rc = po::gemm_run(plan, epi, args, st);
+  if (args.split_ws) cudaFreeAsync(args.split_ws, st);
   if (rc) return po::set_error(PO_ERR_CUDA, "po_op_gemm: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return PO_OK;
 }

@@ -51,6 +51,8 @@ struct po_engine {
   __nv_bfloat16* qkv = nullptr;
   __nv_bfloat16* act = nullptr;
   float2* rope = nullptr;
+  float* gemm_ws = nullptr;  // split-K partials for small-M (prefix-hit) GEMMs
+  size_t gemm_ws_bytes = 0;
   void* attn_ws = nullptr;  // split-KV partials for short-query (prefix-hit) requests
   size_t attn_ws_bytes = 0;
   CUtensorMap map_xn, map_ctx, map_act;
@@ -247,6 +249,16 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       ws = std::max(ws, po::attention_workspace_bytes((int)T, (int)T - nq, c.n_heads, c.n_kv_heads));
     e->attn_ws_bytes = ws;
     if (ws && dalloc(e, &e->attn_ws, ws, &e->arena_bytes)) return fail(PO_ERR_CUDA, "attention workspace failed");
+    // split-K workspace: largest need over the layer GEMM shapes for every M that triggers splitting
+    size_t gw = 0;
+    for (int m = 1; m <= 148 * 128 && m <= T; m += 16) {
+      gw = std::max(gw, po::gemm_split_ws_bytes(m, qkvc, h));
+      gw = std::max(gw, po::gemm_split_ws_bytes(m, h, ctxc));
+      gw = std::max(gw, po::gemm_split_ws_bytes(m, 2 * I, h));
+      gw = std::max(gw, po::gemm_split_ws_bytes(m, h, I));
+    }
+    e->gemm_ws_bytes = gw;
+    if (gw && dalloc(e, &e->gemm_ws, gw, &e->arena_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
   }
   const long long max_blocks = T / c.block_tokens + 1;
   if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
@@ -461,6 +473,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.M = n_miss; g.N = qkvc; g.K = h;
     g.out = e->qkv + (size_t)n_c * qkvc; g.ldo = qkvc;
     g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
+    g.split_ws = e->gemm_ws;
     mark(KC_QKV, true);
     rc |= po::gemm_launch(e->map_xn, ly.map_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
@@ -471,32 +484,38 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       mark(KC_SCATTER, false);
       ++launches;
     }
+    // the last layer only needs the final row's output (the LM head reads nothing else); its K/V rows
+    // were computed (and admitted to the pool) above
+    const bool last_only = c.last_row_only && l == L - 1 && n_miss > 1;
+    const int q_first = last_only ? n - 1 : n_c;       // first query position this layer computes
+    const int rows = n - q_first;                      // query rows of attention / O / MLP
+    const int row0 = q_first - n_c;                    // their offset inside the miss rows
     mark(KC_ATTN, true);
-    rc |= po::attention_run(e->qkv, qkvc, n, n_c, c.n_heads, c.n_kv_heads, e->xn, ctxc, s, e->attn_ws,
+    rc |= po::attention_run(e->qkv, qkvc, n, q_first, c.n_heads, c.n_kv_heads, e->xn, ctxc, s, e->attn_ws,
                             e->attn_ws_bytes);
     mark(KC_ATTN, false);
     ++launches;
     po::GemmArgs go{};
-    go.M = n_miss; go.N = h; go.K = ctxc;
-    go.resid = e->resid; go.ldr = h;
+    go.M = rows; go.N = h; go.K = ctxc;
+    go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
     mark(KC_O, true);
     rc |= po::gemm_launch(e->map_ctx, ly.map_o, po::EPI_RESID_F32, go, s);
     mark(KC_O, false);
     ++launches;
-    for (int lo = 0; lo < n_miss && !rc; lo += c.chunk) {
-      const int rows = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
+    for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
+      const int cr = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
       mark(KC_NORM, true);
-      po::launch_rmsnorm(e->resid + (size_t)lo * h, rows, h, ly.mlp_norm, c.rms_eps, e->xn + (size_t)lo * h, s);
+      po::launch_rmsnorm(e->resid + (size_t)lo * h, cr, h, ly.mlp_norm, c.rms_eps, e->xn + (size_t)lo * h, s);
       mark(KC_NORM, false);
       po::GemmArgs gu{};
-      gu.M = rows; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
-      gu.out = e->act; gu.ldo = I;
+      gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
+      gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
       mark(KC_GATE_UP, true);
       rc |= po::gemm_launch(e->map_xn, ly.map_gu, po::EPI_SILU_MUL, gu, s);
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
-      gd.M = rows; gd.N = h; gd.K = I;
-      gd.resid = e->resid + (size_t)lo * h; gd.ldr = h;
+      gd.M = cr; gd.N = h; gd.K = I;
+      gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
       mark(KC_DOWN, true);
       rc |= po::gemm_launch(e->map_act, ly.map_down, po::EPI_RESID_F32, gd, s);
       mark(KC_DOWN, false);

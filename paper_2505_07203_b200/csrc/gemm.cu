@@ -103,8 +103,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = lane_id();
   const int num_m = (args.M + BM - 1) / BM;
   const int num_n = args.N / BN;
-  const int num_tiles = num_m * num_n;
-  const int nk = args.K / BK;
+  const int ksp = args.k_splits > 1 ? args.k_splits : 1;
+  const int num_tiles = num_m * num_n * ksp;
+  const int nk_total = args.K / BK;
+  const int kbps = ksp > 1 ? args.kb_per_split : nk_total;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -131,8 +133,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, num_m, num_n, mb, nb);
-        for (int kb = 0; kb < nk; ++kb) {
+        tile_coords(t / ksp, num_m, num_n, mb, nb);
+        const int kb0 = (t % ksp) * kbps;
+        const int nk = min(nk_total, kb0 + kbps) - kb0;
+        for (int k = 0; k < nk; ++k) {
+          const int kb = kb0 + k;
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
           tma_load_2d(sA + s * A_BYTES, &map_a, &full_bar[s], kb * BK, args.a_row0 + mb * BM);
@@ -154,6 +159,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        const int kb0 = (t % ksp) * kbps;
+        const int nk = min(nk_total, kb0 + kbps) - kb0;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
@@ -176,14 +183,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      tile_coords(t / ksp, num_m, num_n, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
       const int row = mb * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      if constexpr (EPI == EPI_QKV_ROPE) {
+      if (ksp > 1) {
+        // split-K partial: raw fp32 tile into the workspace slice of this split
+        GemmArgs pa = args;
+        pa.out = args.split_ws + (size_t)(t % ksp) * args.M * args.N;
+        pa.ldo = args.N;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_ld_wait();
+          if (row < args.M) epilogue_chunk<EPI_F32>(pa, row, nb * BN + c, r);
+        }
+      } else if constexpr (EPI == EPI_QKV_ROPE) {
         // two 128-column heads per tile; rotate-half pairs (i, i+64)
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
@@ -231,6 +250,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// Split-K reduction: sum the partials in split order, then apply the epilogue (one thread per 4 columns).
+template <int EPI>
+__global__ void splitk_reduce_kernel(const GemmArgs a) {
+  const int ncol4 = a.N / 4;
+  const long long total = (long long)a.M * ncol4;
+  const size_t slice = (size_t)a.M * a.N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(i / ncol4);
+    const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
+    const float* p = a.split_ws + (size_t)row * a.N + col;
+    float4 acc = *reinterpret_cast<const float4*>(p);
+    for (int s = 1; s < a.k_splits; ++s) {
+      const float4 v = *reinterpret_cast<const float4*>(p + s * slice);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if constexpr (EPI == EPI_BF16) {
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
+          make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+    } else if constexpr (EPI == EPI_F32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(a.out) + (long long)row * a.ldo + col) = acc;
+    } else if constexpr (EPI == EPI_RESID_F32) {
+      float4* d = reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col);
+      float4 v = *d;
+      v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
+      *d = v;
+    } else if constexpr (EPI == EPI_SILU_MUL) {
+      // 16-column groups: [gate 16 | up 16]; this thread's 4 columns are gate or up of output cols
+      const int grp = col / 32, w = col % 32;
+      if (w < 16) {
+        float4 up = *reinterpret_cast<const float4*>(p + 16);
+        for (int s = 1; s < a.k_splits; ++s) {
+          const float4 v = *reinterpret_cast<const float4*>(p + 16 + s * slice);
+          up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
+        }
+        const int oc = grp * 16 + w;
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
+            make_uint2(pack_bf16(silu_f(acc.x) * up.x, silu_f(acc.y) * up.y),
+                       pack_bf16(silu_f(acc.z) * up.z, silu_f(acc.w) * up.w));
+      }
+    } else if constexpr (EPI == EPI_QKV_ROPE) {
+      const int head_col = col % 128;
+      if (col < a.rope_cols && head_col < 64) {
+        float4 x2 = *reinterpret_cast<const float4*>(p + 64);
+        for (int s = 1; s < a.k_splits; ++s) {
+          const float4 v = *reinterpret_cast<const float4*>(p + 64 + s * slice);
+          x2.x += v.x; x2.y += v.y; x2.z += v.z; x2.w += v.w;
+        }
+        const float2* cs = a.rope + (long long)(a.pos_offset + row) * 64 + head_col;
+        const float4 x1 = acc;
+        const float2 c0 = cs[0], c1 = cs[1], c2 = cs[2], c3 = cs[3];
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col;
+        *reinterpret_cast<uint2*>(o) =
+            make_uint2(pack_bf16(x1.x * c0.x - x2.x * c0.y, x1.y * c1.x - x2.y * c1.y),
+                       pack_bf16(x1.z * c2.x - x2.z * c2.y, x1.w * c3.x - x2.w * c3.y));
+        *reinterpret_cast<uint2*>(o + 64) =
+            make_uint2(pack_bf16(x2.x * c0.x + x1.x * c0.y, x2.y * c1.x + x1.y * c1.y),
+                       pack_bf16(x2.z * c2.x + x1.z * c2.y, x2.w * c3.x + x1.w * c3.y));
+      } else if (col >= a.rope_cols) {
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
+            make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+      }
+    }
   }
 }
 
@@ -289,16 +374,50 @@ int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long 
   return 0;
 }
 
+static void split_plan(int M, int N, int K, int* splits, int* kbps) {
+  const int tiles_mn = ((M + BM - 1) / BM) * (N / BN);
+  const int nk = K / BK;
+  int s = 1;
+  if (tiles_mn * 2 <= num_sms() && nk >= 16) {
+    s = num_sms() / tiles_mn;
+    s = s < nk / 8 ? s : nk / 8;
+    s = s > 1 ? s : 1;
+  }
+  *kbps = (nk + s - 1) / s;
+  *splits = (nk + *kbps - 1) / *kbps;
+}
+
+size_t gemm_split_ws_bytes(int M, int N, int K) {
+  int s, kbps;
+  split_plan(M, N, K, &s, &kbps);
+  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
+}
+
 template <int EPI>
-static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmArgs& args, cudaStream_t stream) {
+static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmArgs& in, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     configured = true;
   }
-  const int tiles = ((args.M + BM - 1) / BM) * (args.N / BN);
+  GemmArgs args = in;
+  args.k_splits = 1;
+  if (args.split_ws) {
+    int s, kbps;
+    split_plan(args.M, args.N, args.K, &s, &kbps);
+    if (s > 1) {
+      args.k_splits = s;
+      args.kb_per_split = kbps;
+    }
+  }
+  const int tiles = ((args.M + BM - 1) / BM) * (args.N / BN) * args.k_splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_kernel<EPI><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(map_a, map_b, args);
+  if (args.k_splits > 1) {
+    const long long total = (long long)args.M * (args.N / 4);
+    const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+    splitk_reduce_kernel<EPI><<<blocks, 256, 0, stream>>>(args);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 

@@ -22,6 +22,11 @@ struct GemmArgs {
   const float2* rope;   // [pos][64] (cos, sin) for EPI_QKV_ROPE
   int pos_offset;       // absolute position of row 0
   int rope_cols;        // columns [0, rope_cols) are rotated (q and k heads)
+  // split-K (small-M GEMMs, e.g. prefix-hit requests): k_splits > 1 writes fp32 partials to `split_ws`
+  // ([k_splits][M][N]) and a reduce kernel applies the epilogue after summing in a fixed order.
+  int k_splits;
+  int kb_per_split;
+  float* split_ws;
 };
 
 struct GemmPlan {
@@ -38,6 +43,8 @@ int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& args, cudaStream_t s
 // A/B maps built once (weights at init, activation buffers at init with their max rows).
 int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, const GemmArgs& args,
                 cudaStream_t stream);
+// Workspace bytes a launch of this shape needs for split-K (0 = no split).
+size_t gemm_split_ws_bytes(int M, int N, int K);
 int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, int K);
 int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int num_sms();

@@ -55,7 +55,7 @@ class Engine:
 
     def __init__(self, model: ModelConfig | str = "llama-3.1-8b", device: int = 0, seed: int = 0,
                  max_tokens: int = 32_768, chunk: int = DEFAULT_CHUNK, block_tokens: int = BLOCK_TOKENS,
-                 pool_blocks: int = -1, pool_mem_fraction: float = 0.9):
+                 pool_blocks: int = -1, pool_mem_fraction: float = 0.9, last_row_only: bool = True):
         self.model = get_preset(model) if isinstance(model, str) else model
         self.device = device
         self.seed = seed
@@ -63,7 +63,8 @@ class Engine:
         self.chunk = chunk
         self.block_tokens = block_tokens
         lib = _lib.load()
-        cfg = to_c_cfg(self.model, max_tokens, chunk, block_tokens, pool_blocks, pool_mem_fraction)
+        self.last_row_only = last_row_only
+        cfg = to_c_cfg(self.model, max_tokens, chunk, block_tokens, pool_blocks, pool_mem_fraction, last_row_only)
         handle = ctypes.c_void_p()
         try:
             _lib.check(lib.po_init(device, ctypes.addressof(cfg), seed, ctypes.addressof(handle)))

@@ -127,6 +127,16 @@ def test_admission_writes_pool_then_long_hit(tiny_engine):
     check_against_oracle(TINY, res, base, YES_NO, 42)
 
 
+def test_last_row_only_equals_full_last_layer():
+    toks = tokens_for(31, 1700)
+    res = {}
+    for flag in (True, False):
+        with Engine(TINY, seed=42, max_tokens=2048, chunk=512, pool_blocks=8, last_row_only=flag) as e:
+            res[flag] = e.prefill(toks, YES_NO)
+            check_against_oracle(TINY, res[flag], toks, YES_NO, 42)
+    assert np.abs(res[True].logits - res[False].logits).max() <= LOGIT_ATOL
+
+
 def test_capacity_error(tiny_engine):
     with pytest.raises(CapacityError):
         tiny_engine.prefill(tokens_for(0, 4097), YES_NO)

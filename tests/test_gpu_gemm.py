@@ -124,3 +124,57 @@ def test_gemm_rejects_bad_shape():
     out = torch.empty(64, 100, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(_lib.PrefillOnlyError):
         _gemm(A, B, out)
+
+
+# ---- split-K path (small M, long K: prefix-hit requests); partials summed in a fixed order, then the epilogue
+@pytest.mark.parametrize("M,N,K", [(160, 6144, 4096), (1, 4096, 4096), (150, 4096, 14336), (300, 1024, 8192)])
+def test_splitk_bf16_and_resid(M, N, K):
+    torch.manual_seed(M + K)
+    A = _rand(M, K)
+    B = _rand(N, K, scale=K ** -0.5)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, B, out)
+    ref = A.float() @ B.float().T
+    assert _rel(out, ref) < TOL_BF16
+    resid = torch.randn(M, N, device="cuda")
+    base = resid.clone()
+    _gemm(A, B, resid=resid, epi=_lib.EPI_RESID_F32)
+    assert _rel(resid, base + ref) < TOL_F32
+
+
+def test_splitk_silu_mul():
+    torch.manual_seed(8)
+    M, I, K = 150, 2048, 4096
+    A = _rand(M, K)
+    gate = _rand(I, K, scale=K ** -0.5)
+    up = _rand(I, K, scale=K ** -0.5)
+    W = torch.stack([gate.view(I // 16, 16, K), up.view(I // 16, 16, K)], dim=1).reshape(2 * I, K).contiguous()
+    out = torch.empty(M, I, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, W, out, epi=_lib.EPI_SILU_MUL)
+    g = A.float() @ gate.float().T
+    u = A.float() @ up.float().T
+    assert _rel(out, g / (1 + torch.exp(-g)) * u) < TOL_BF16
+
+
+def test_splitk_qkv_rope():
+    torch.manual_seed(9)
+    M, K, hd = 150, 4096, 128
+    nq, nkv = 8, 2
+    N = (nq + 2 * nkv) * hd
+    A = _rand(M, K)
+    B = _rand(N, K, scale=K ** -0.5)
+    pos_offset = 19850
+    pos = torch.arange(pos_offset + M, dtype=torch.float32)
+    inv = 1.0 / (500000.0 ** (torch.arange(0, hd, 2, dtype=torch.float32) / hd))
+    ang = pos[:, None] * inv[None, :]
+    table = torch.stack([torch.cos(ang), torch.sin(ang)], dim=-1).contiguous().cuda()
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    rope_cols = (nq + nkv) * hd
+    _gemm(A, B, out, epi=_lib.EPI_QKV_ROPE, rope=table, pos_offset=pos_offset, rope_cols=rope_cols)
+    y = (A.float() @ B.float().T).view(M, -1, hd)
+    c = table[pos_offset:pos_offset + M, :, 0][:, None, :]
+    s = table[pos_offset:pos_offset + M, :, 1][:, None, :]
+    x1, x2 = y[..., :64], y[..., 64:]
+    rot = torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
+    ref = torch.cat([rot[:, :rope_cols // hd], y[:, rope_cols // hd:]], dim=1).reshape(M, N)
+    assert _rel(out, ref) < TOL_BF16
