@@ -35,6 +35,12 @@ constexpr int TILE_BYTES = 2 * BOX_BYTES;      // 128 x 128 bf16
 constexpr int NTHREADS = 384;
 constexpr int SMEM_BYTES = 6 * TILE_BYTES + 1024 + 256;
 constexpr float RESCALE_THRESHOLD = 8.0f;      // log2 units
+#ifndef POLY_NUM
+#define POLY_NUM 1  // POLY_NUM of every POLY_DEN exp2 pairs run as the FMA-pipe polynomial (MUFU offload)
+#endif
+#ifndef POLY_DEN
+#define POLY_DEN 4
+#endif
 }  // namespace
 
 struct AttnArgs {
@@ -51,6 +57,47 @@ struct AttnArgs {
   float* part_o;      // [splits][n_q][hq*128] unnormalised fp32 partial outputs (splits > 1)
   float2* part_ml;    // [splits][n_q][hq] (running max in log2 units, running sum)
 };
+
+// ---- packed f32x2 math (sm_100 FFMA2 / FADD2) and a polynomial exp2 on the FMA pipe (MUFU offload)
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair, x <= ~8: Cody-Waite split x = j + f (j = rint(x), |f| <= 1/2), cubic minimax for 2^f
+// (max rel. error 7.5e-5, far below the bf16 rounding of P), exponent add for 2^j. x is clamped at -125.
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float& y1) {
+  const float MAGIC = 12582912.0f;  // 1.5 * 2^23: adding it rounds to an integer held in the low bits
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  const uint64_t x = pk2(x0, x1);
+  const uint64_t t = fadd2(x, pk2(MAGIC, MAGIC));
+  const uint64_t f = fsub2(x, fsub2(t, pk2(MAGIC, MAGIC)));
+  uint64_t p = ffma2(pk2(0.05517098f, 0.05517098f), f, pk2(0.2426097f, 0.2426097f));
+  p = ffma2(p, f, pk2(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, pk2(0.99992818f, 0.99992818f));
+  float p0, p1, t0, t1;
+  up2(p, p0, p1);
+  up2(t, t0, t1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
 
 // One 128-key tile of online softmax for this thread's query row (TMEM lane): reads S, writes P (bf16,
 // packed over the first 64 columns of S), keeps (m, l). `lim` = number of visible keys in the tile
@@ -99,7 +146,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
     m = m_new;
   }
   const float nm = -m;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(nm, nm);
+  uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
 #pragma unroll
   for (int c = 0; c < 4; c += 2) {
     uint32_t v0[32], v1[32];
@@ -109,20 +157,27 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
     uint32_t p0[16], p1[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      float x0 = ex2_approx(fmaf(__uint_as_float(v0[2 * e]), sl2, nm));
-      float x1 = ex2_approx(fmaf(__uint_as_float(v0[2 * e + 1]), sl2, nm));
-      float y0 = ex2_approx(fmaf(__uint_as_float(v1[2 * e]), sl2, nm));
-      float y1 = ex2_approx(fmaf(__uint_as_float(v1[2 * e + 1]), sl2, nm));
+      float x0, x1, y0, y1;
+      up2(ffma2(pk2(__uint_as_float(v0[2 * e]), __uint_as_float(v0[2 * e + 1])), sc2, nm2), x0, x1);
+      up2(ffma2(pk2(__uint_as_float(v1[2 * e]), __uint_as_float(v1[2 * e + 1])), sc2, nm2), y0, y1);
+      if (!MASKED && (e % POLY_DEN) >= POLY_DEN - POLY_NUM) {
+        // one pair in four per chunk goes through the FMA-pipe polynomial: MUFU and FMA pipes share the load
+        exp2_poly2(x0, x1, x0, x1);
+        exp2_poly2(y0, y1, y0, y1);
+      } else {
+        x0 = ex2_approx(x0);
+        x1 = ex2_approx(x1);
+        y0 = ex2_approx(y0);
+        y1 = ex2_approx(y1);
+      }
       if (MASKED) {
         if (c * 32 + 2 * e >= lim) x0 = 0.f;
         if (c * 32 + 2 * e + 1 >= lim) x1 = 0.f;
         if ((c + 1) * 32 + 2 * e >= lim) y0 = 0.f;
         if ((c + 1) * 32 + 2 * e + 1 >= lim) y1 = 0.f;
       }
-      s0 += x0;
-      s1 += x1;
-      s2 += y0;
-      s3 += y1;
+      acc0 = fadd2(acc0, pk2(x0, x1));
+      acc1 = fadd2(acc1, pk2(y0, y1));
       p0[e] = pack_bf16(x0, x1);
       p1[e] = pack_bf16(y0, y1);
     }
@@ -130,6 +185,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
     tmem_st16(s_addr + c * 16, p0);
     tmem_st16(s_addr + (c + 1) * 16, p1);
   }
+  float s0, s1, s2, s3;
+  up2(acc0, s0, s1);
+  up2(acc1, s2, s3);
   l += (s0 + s1) + (s2 + s3);
 }
 
