@@ -83,6 +83,7 @@ typedef struct po_model_cfg {
   double pool_mem_fraction;  /* profile run: fraction of HBM left after the arena given to the pool    */
   int32_t last_row_only;     /* 1: in the last layer run attention/O/MLP for the final row only (exact:    */
                              /*    only that row reaches the LM head); 0: every row through every layer  */
+  int32_t qkv_bias;          /* 1: q/k/v projections carry a bias (Qwen2), added before RoPE               */
 } po_model_cfg;
 
 typedef struct po_engine po_engine;
@@ -129,7 +130,7 @@ int po_engine_info(po_engine* e, int64_t* out, int32_t n);
 
 /* Overwrite one weight tensor from host memory (logical, un-interleaved layout; bf16 except norms = fp32).
  * kind: 0 embed, 1 attn_norm, 2 wq, 3 wk, 4 wv, 5 wo, 6 mlp_norm, 7 w_gate, 8 w_up, 9 w_down, 10 final_norm,
- * 11 lm_head. */
+ * 11 lm_head, 12 qkv bias (fp32, [(Hq+2Hkv)*128]). */
 int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, int64_t nelem);
 
 #ifdef __cplusplus

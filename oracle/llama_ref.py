@@ -29,7 +29,7 @@ K_SEED = np.uint64(0x9E3779B97F4A7C15)
 K_TID = np.uint64(0xD1B54A32D192ED03)
 SQRT3_F32 = np.float32(1.7320508)
 TID_EMBED, TID_FINAL_NORM, TID_LM_HEAD = 0xFFFF0, 0xFFFF1, 0xFFFF2
-K_ATTN_NORM, K_Q, K_K, K_V, K_O, K_MLP_NORM, K_GATE, K_UP, K_DOWN = range(9)
+K_ATTN_NORM, K_Q, K_K, K_V, K_O, K_MLP_NORM, K_GATE, K_UP, K_DOWN, K_QKV_BIAS = range(10)
 
 
 def bf16_round(x) -> np.ndarray:
@@ -77,6 +77,11 @@ def init_norm(seed: int, tid: int, n: int) -> np.ndarray:
     return bf16_round(np.float32(1.0) + np.float32(0.05) * u)
 
 
+def init_bias(seed: int, tid: int, n: int) -> np.ndarray:
+    """bf16(0.1 * u) (init_bias_kernel)."""
+    return bf16_round(np.float32(0.1) * unit_uniform(seed, tid, np.arange(n, dtype=np.uint64)))
+
+
 def layer_tid(layer: int, kind: int) -> int:
     return layer * 16 + kind
 
@@ -100,6 +105,7 @@ class Cfg:
     rope_low_freq_factor: float = 1.0
     rope_high_freq_factor: float = 4.0
     rope_original_max_pos: int = 8192
+    qkv_bias: bool = False
 
     @classmethod
     def from_model(cls, m) -> "Cfg":
@@ -127,6 +133,8 @@ def make_weights(cfg: Cfg, seed: int) -> dict:
             "w_up": init_matrix(seed, layer_tid(l, K_UP), i_, h, fan_scale(h)),
             "w_down": init_matrix(seed, layer_tid(l, K_DOWN), h, i_, fan_scale(i_)),
         })
+        if cfg.qkv_bias:
+            w["layers"][-1]["bqkv"] = init_bias(seed, layer_tid(l, K_QKV_BIAS), (cfg.n_heads + 2 * cfg.n_kv_heads) * hd)
     return w
 
 
@@ -260,9 +268,13 @@ def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_
     x = w["embed"][toks.astype(np.int64)].astype(np.float64)
     for lw in w["layers"]:
         xn = rmsnorm(x, lw["attn_norm"], cfg.rms_eps, R)
-        q = (xn @ lw["wq"].T.astype(np.float64)).reshape(n, hq, hd)
-        k = (xn @ lw["wk"].T.astype(np.float64)).reshape(n, hkv, hd)
-        v = (xn @ lw["wv"].T.astype(np.float64)).reshape(n, hkv, hd)
+        q = xn @ lw["wq"].T.astype(np.float64)
+        k = xn @ lw["wk"].T.astype(np.float64)
+        v = xn @ lw["wv"].T.astype(np.float64)
+        if "bqkv" in lw:  # Qwen2: bias added to the projections before RoPE
+            b = lw["bqkv"].astype(np.float64)
+            q, k, v = q + b[: hq * hd], k + b[hq * hd:(hq + hkv) * hd], v + b[(hq + hkv) * hd:]
+        q, k, v = q.reshape(n, hq, hd), k.reshape(n, hkv, hd), v.reshape(n, hkv, hd)
         q = R(apply_rope(q, cos, sin))
         k = R(apply_rope(k, cos, sin))
         v = R(v)

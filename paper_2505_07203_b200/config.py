@@ -32,6 +32,7 @@ class ModelConfig:
     rope_low_freq_factor: float = 1.0
     rope_high_freq_factor: float = 4.0
     rope_original_max_pos: int = 8192
+    qkv_bias: bool = False  # Qwen2-style q/k/v projection bias
 
     @property
     def kv_bytes_per_token(self) -> tuple[int, int]:
@@ -50,8 +51,10 @@ class ModelConfig:
     def linear_flops_per_token(self) -> float:
         """Dense-layer FLOPs per token over all layers (ps/costs.py:126-131)."""
         h = self.hidden
+        q_dim = self.n_heads * self.head_dim
         kv_dim = self.n_kv_heads * self.head_dim
-        per_layer = 2.0 * (h * (h + 2 * kv_dim) + h * h + 3 * h * self.intermediate)
+        # reference formula (ps/costs.py:126-131) assumes q_dim == h; stated generally here (equal for Llama/Qwen)
+        per_layer = 2.0 * (h * (q_dim + 2 * kv_dim) + q_dim * h + 3 * h * self.intermediate)
         return self.num_layers * per_layer
 
     def attn_flops_per_pair(self) -> float:
@@ -69,11 +72,10 @@ class ModelConfig:
 LLAMA_3_1_8B = ModelConfig("llama-3.1-8b", 32, 4096, 32, 8, 128, 14336, 128_256)
 # Tiny parity config (BASELINE.json configs[0]): 2 layers, d=256, GQA 2:1, build-chosen and stated.
 TINY = ModelConfig("tiny", 2, 256, 2, 1, 128, 1024, 32_000)
-# Qwen-2.5-32B shapes (Qwen/Qwen2.5-32B config.json), rope theta 1e6, eps 1e-6, no rope scaling.
-# Note: 40 query / 8 kv heads is an odd GQA group (5); the attention kernel pairs heads within a group,
-# so this preset is declared for sizing and is rejected by po_init until odd groups are supported.
+# Qwen-2.5-32B shapes (Qwen/Qwen2.5-32B config.json): rope theta 1e6, eps 1e-6, no rope scaling, q/k/v
+# bias. 40 query / 8 kv heads is an odd GQA group (5): attention runs two query blocks of one head per CTA.
 QWEN_2_5_32B = ModelConfig("qwen-2.5-32b", 64, 5120, 40, 8, 128, 27648, 152_064, rms_eps=1e-6,
-                           rope_theta=1_000_000.0, rope_scaling=0)
+                           rope_theta=1_000_000.0, rope_scaling=0, qkv_bias=True)
 
 PRESETS = {c.name: c for c in (TINY, LLAMA_3_1_8B, QWEN_2_5_32B)}
 
@@ -109,6 +111,7 @@ class PoModelCfg(ctypes.Structure):
         ("pool_blocks", ctypes.c_int64),
         ("pool_mem_fraction", ctypes.c_double),
         ("last_row_only", ctypes.c_int32),
+        ("qkv_bias", ctypes.c_int32),
     ]
 
 
@@ -116,6 +119,7 @@ def to_c_cfg(model: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK, bl
              pool_blocks: int = -1, pool_mem_fraction: float = 0.9, last_row_only: bool = True) -> PoModelCfg:
     d = asdict(model)
     d.pop("name")
+    d["qkv_bias"] = int(d["qkv_bias"])
     return PoModelCfg(**d, max_tokens=max_tokens, chunk=chunk, block_tokens=block_tokens, pool_blocks=pool_blocks,
                       pool_mem_fraction=pool_mem_fraction, last_row_only=int(last_row_only))
 

@@ -56,6 +56,8 @@ struct AttnArgs {
   int tiles_per_split;
   float* part_o;      // [splits][n_q][hq*128] unnormalised fp32 partial outputs (splits > 1)
   float2* part_ml;    // [splits][n_q][hq] (running max in log2 units, running sum)
+  int qpair;          // 0: the two TMEM slots hold two query heads of one GQA group (even groups)
+                      // 1: they hold two consecutive 128-row query blocks of one head (any group, e.g. 40/8)
 };
 
 // ---- packed f32x2 math (sm_100 FFMA2 / FADD2) and a polynomial exp2 on the FMA pipe (MUFU offload)
@@ -211,16 +213,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = warp_id();
   const int lane = lane_id();
 
-  // heaviest (longest causal extent) query blocks first
-  const int per_qb = a.hkv * a.pairs * a.splits;
-  const int qb = a.num_qb - 1 - blockIdx.x / per_qb;
-  int rem = blockIdx.x % per_qb;
-  const int split = rem % a.splits;
-  rem /= a.splits;
-  const int g = rem / a.pairs;
-  const int h0 = g * (2 * a.pairs) + 2 * (rem % a.pairs);
-  const int q_lo = a.q_offset + qb * BQ;                    // position of query row 0 of this block
-  const int q_hi = min(q_lo + BQ - 1, a.n_total - 1);       // last real query position
+  // heaviest (longest causal extent) query blocks first. Slot i of this CTA: head hs_i, first position qs_i.
+  int split, g, hs0, hs1, qs0, qs1;
+  if (!a.qpair) {
+    const int per_qb = a.hkv * a.pairs * a.splits;
+    const int qb = a.num_qb - 1 - blockIdx.x / per_qb;
+    int rem = blockIdx.x % per_qb;
+    split = rem % a.splits;
+    rem /= a.splits;
+    g = rem / a.pairs;
+    hs0 = g * (2 * a.pairs) + 2 * (rem % a.pairs);
+    hs1 = hs0 + 1;
+    qs0 = qs1 = a.q_offset + qb * BQ;
+  } else {
+    const int per = a.hq * a.splits;
+    const int qb2 = (a.num_qb + 1) / 2 - 1 - blockIdx.x / per;
+    const int rem = blockIdx.x % per;
+    split = rem % a.splits;
+    hs0 = hs1 = rem / a.splits;
+    g = hs0 / (a.hq / a.hkv);
+    qs0 = a.q_offset + qb2 * 2 * BQ;
+    qs1 = qs0 + BQ;
+  }
+  const int q_lo = qs0;                                     // earliest query position of the CTA
+  const int q_hi = min(qs1 + BQ - 1, a.n_total - 1);        // last real query position of the CTA
   const int all_tiles = q_hi / BKV + 1;
   const int t0 = split * a.tiles_per_split;                 // this CTA's KV tile range [t0, t0 + n_tiles)
   const int n_tiles = max(0, min(all_tiles, t0 + a.tiles_per_split) - t0);
@@ -246,7 +262,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int half = 0; half < 2; ++half)
-          tma_load_2d(sQ + i * TILE_BYTES + half * BOX_BYTES, &map, q_full, (h0 + i) * HD + half * 64, q_lo);
+          tma_load_2d(sQ + i * TILE_BYTES + half * BOX_BYTES, &map, q_full, (i ? hs1 : hs0) * HD + half * 64,
+                      i ? qs1 : qs0);
       const int kcol = a.hq * HD + g * HD;
       const int vcol = (a.hq + a.hkv) * HD + g * HD;
       for (int j = 0; j < n_tiles; ++j) {
@@ -319,7 +336,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + i * 128;
     const uint32_t o_addr = tmem + lane_base + 256 + i * 128;
-    const int pos = q_lo + r;
+    const int my_qlo = i ? qs1 : qs0;
+    const int my_h = i ? hs1 : hs0;
+    const int pos = my_qlo + r;
     float m = -INFINITY;  // running max (scaled, log2 units), possibly stale
     float l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
@@ -327,7 +346,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_after();
       const int kbase = (t0 + j) * BKV;
       // warp-uniform: only tiles crossing the diagonal of this query block pay for the mask
-      if (kbase + BKV - 1 > q_lo) {
+      if (kbase + BKV - 1 > my_qlo) {
         softmax_tile<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l);
       } else {
         softmax_tile<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l);
@@ -338,10 +357,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     mbar_wait(&o_final[i], 0);
     tc_fence_after();
-    const int row = qb * BQ + r;
+    const int row = my_qlo - a.q_offset + r;
     if (a.splits == 1) {
       const float inv = 1.0f / l;
-      __nv_bfloat16* dst = a.out + (long long)row * a.ldo + (h0 + i) * HD;
+      __nv_bfloat16* dst = a.out + (long long)row * a.ldo + my_h * HD;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
@@ -361,7 +380,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
       // split-KV partial: unnormalised O, running max m (log2 units) and sum l for the combine kernel
       const long long prow = (long long)split * a.n_q + row;
-      float4* dst = reinterpret_cast<float4*>(a.part_o + prow * (a.hq * HD) + (h0 + i) * HD);
+      float4* dst = reinterpret_cast<float4*>(a.part_o + prow * (a.hq * HD) + my_h * HD);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
@@ -374,7 +393,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
         }
       }
-      if (row < a.n_q) a.part_ml[prow * a.hq + h0 + i] = make_float2(m, l);
+      if (row < a.n_q) a.part_ml[prow * a.hq + my_h] = make_float2(m, l);
     }
   }
 
@@ -388,7 +407,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 // out[row, h, :] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s over the KV splits that exist for the row's block
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml, int n_q,
-                                    int hq, int splits, int tiles_per_split, int q_offset, int n_total,
+                                    int hq, int splits, int tiles_per_split, int q_offset, int n_total, int qpair,
                                     __nv_bfloat16* __restrict__ out, long long ldo) {
   const long long total = (long long)n_q * hq * (HD / 4);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -397,8 +416,8 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o, const floa
     const long long rh = i / (HD / 4);
     const int h = static_cast<int>(rh % hq);
     const int row = static_cast<int>(rh / hq);
-    const int qb = row / BQ;
-    const int q_hi = min(q_offset + qb * BQ + BQ - 1, n_total - 1);
+    const int span = qpair ? 2 * BQ : BQ;  // query rows per CTA
+    const int q_hi = min(q_offset + (row / span) * span + span - 1, n_total - 1);
     const int all_tiles = q_hi / BKV + 1;
     const int ns = min(splits, (all_tiles + tiles_per_split - 1) / tiles_per_split);
     float M = -INFINITY;
@@ -425,7 +444,8 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o, const floa
 void attention_split_plan(int n_total, int q_offset, int hq, int hkv, int* splits, int* tiles_per_split) {
   const int n_q = n_total - q_offset;
   const int num_qb = (n_q + BQ - 1) / BQ;
-  const int base = num_qb * hkv * (hq / hkv / 2);
+  const bool qpair = (hq / hkv) % 2 != 0;
+  const int base = qpair ? ((num_qb + 1) / 2) * hq : num_qb * hkv * (hq / hkv / 2);
   const int max_tiles = (n_total - 1) / BKV + 1;
   int s = 1;
   if (base < 148 && max_tiles >= 8) {
@@ -449,7 +469,7 @@ size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv) {
 
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
                   cudaStream_t stream, void* workspace, size_t workspace_bytes) {
-  if (hq % hkv || (hq / hkv) % 2) return -3;
+  if (hq % hkv) return -3;
   CUtensorMap map;
   if (make_tmap_2d_bf16(&map, qkv, ld, n_total, ld * 2, 64, 128)) return -2;
   static bool configured = false;
@@ -463,7 +483,8 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
   a.n_q = n_total - q_offset;
   a.hq = hq;
   a.hkv = hkv;
-  a.pairs = hq / hkv / 2;
+  a.qpair = (hq / hkv) % 2 != 0;
+  a.pairs = a.qpair ? 1 : hq / hkv / 2;
   a.num_qb = (a.n_q + BQ - 1) / BQ;
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
@@ -479,13 +500,13 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
     a.part_ml = reinterpret_cast<float2*>(static_cast<char*>(workspace) +
                                           (size_t)a.splits * a.n_q * hq * HD * sizeof(float));
   }
-  const int grid = a.num_qb * hkv * a.pairs * a.splits;
+  const int grid = (a.qpair ? ((a.num_qb + 1) / 2) * hq : a.num_qb * hkv * a.pairs) * a.splits;
   attn_fwd_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(map, a);
   if (a.splits > 1) {
     const long long total = (long long)a.n_q * hq * (HD / 4);
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
     attn_combine_kernel<<<blocks, 256, 0, stream>>>(a.part_o, a.part_ml, a.n_q, hq, a.splits, a.tiles_per_split,
-                                                    q_offset, n_total, a.out, ldo);
+                                                    q_offset, n_total, a.qpair, a.out, ldo);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
@@ -497,8 +518,9 @@ extern "C" int po_op_attention(const void* qkv, int64_t ld, int32_t n_total, int
   if (!qkv || !out) return po::set_error(PO_ERR_ARG, "po_op_attention: null pointer");
   if (n_total <= 0 || q_offset < 0 || q_offset >= n_total)
     return po::set_error(PO_ERR_ARG, "po_op_attention: need 0 <= q_offset < n_total (got %d, %d)", q_offset, n_total);
-  if (n_heads <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads || (n_heads / n_kv_heads) % 2)
-    return po::set_error(PO_ERR_ARG, "po_op_attention: heads %d/%d must give an even GQA group", n_heads, n_kv_heads);
+  if (n_heads <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads)
+    return po::set_error(PO_ERR_ARG, "po_op_attention: heads %d/%d must give an integer GQA group", n_heads,
+                         n_kv_heads);
   if (ld < (int64_t)(n_heads + 2 * n_kv_heads) * 128 || ld % 8)
     return po::set_error(PO_ERR_ARG, "po_op_attention: ld %lld too small or unaligned", (long long)ld);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -42,6 +42,7 @@ struct po_engine {
   struct Layer {
     __nv_bfloat16 *wqkv, *wo, *wgu, *wdown;
     float *attn_norm, *mlp_norm;
+    float* bqkv = nullptr;  // q/k/v bias (qkv_bias models), fp32 holding bf16 values
     CUtensorMap map_qkv, map_o, map_gu, map_down;
   };
   std::vector<Layer> layers;
@@ -96,7 +97,8 @@ using po::set_error;
 
 // tensor ids of the counter-hash init (oracle/llama_ref.py mirrors these)
 constexpr uint32_t TID_EMBED = 0xFFFF0, TID_FINAL_NORM = 0xFFFF1, TID_LM_HEAD = 0xFFFF2;
-enum { K_ATTN_NORM = 0, K_Q = 1, K_K = 2, K_V = 3, K_O = 4, K_MLP_NORM = 5, K_GATE = 6, K_UP = 7, K_DOWN = 8 };
+enum { K_ATTN_NORM = 0, K_Q = 1, K_K = 2, K_V = 3, K_O = 4, K_MLP_NORM = 5, K_GATE = 6, K_UP = 7, K_DOWN = 8,
+       K_QKV_BIAS = 9 };
 inline uint32_t layer_tid(int layer, int kind) { return static_cast<uint32_t>(layer) * 16u + kind; }
 inline float fan_scale(int fan_in) { return static_cast<float>(1.0 / std::sqrt(static_cast<double>(fan_in))); }
 
@@ -140,8 +142,8 @@ int validate_cfg(const po_model_cfg& c) {
       c.vocab <= 0 || c.max_tokens <= 0 || c.chunk <= 0 || c.block_tokens <= 0)
     return set_error(PO_ERR_CONFIG, "po_init: all shape counts must be positive");
   if (c.head_dim != 128) return set_error(PO_ERR_CONFIG, "po_init: head_dim must be 128 (got %d)", c.head_dim);
-  if (c.n_heads % c.n_kv_heads || (c.n_heads / c.n_kv_heads) % 2)
-    return set_error(PO_ERR_CONFIG, "po_init: n_heads/n_kv_heads must be an even integer");
+  if (c.n_heads % c.n_kv_heads)
+    return set_error(PO_ERR_CONFIG, "po_init: n_heads must be a multiple of n_kv_heads");
   if (c.hidden % 256 || c.intermediate % 128 || ((c.n_heads + 2 * c.n_kv_heads) * 128) % 256)
     return set_error(PO_ERR_CONFIG, "po_init: hidden %% 256, intermediate %% 128 and qkv width %% 256 required");
   if (c.hidden > 8192) return set_error(PO_ERR_CONFIG, "po_init: hidden > 8192 unsupported by the LM-head kernel");
@@ -226,6 +228,10 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
                          po::INIT_GATE_UP, s);
     po::launch_init_bf16(ly.wdown, h, I, seed, layer_tid(l, K_DOWN), 0, fan_scale(I), po::INIT_PLAIN, s);
     po::launch_init_norm(ly.attn_norm, h, seed, layer_tid(l, K_ATTN_NORM), s);
+    if (c.qkv_bias) {
+      if (dalloc(e, &ly.bqkv, (size_t)qkvc * 4, &e->weight_bytes)) return fail(PO_ERR_CUDA, "bias allocation failed");
+      po::launch_init_bias(ly.bqkv, qkvc, seed, layer_tid(l, K_QKV_BIAS), s);
+    }
     po::launch_init_norm(ly.mlp_norm, h, seed, layer_tid(l, K_MLP_NORM), s);
     if (po::make_tmap_b(&ly.map_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b(&ly.map_o, ly.wo, ctxc, h, ctxc) ||
         po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I))
@@ -343,13 +349,13 @@ int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, 
   const po_model_cfg& c = e->cfg;
   const int h = c.hidden, I = c.intermediate;
   const int qrows = c.n_heads * c.head_dim, kvrows = c.n_kv_heads * c.head_dim;
-  if (kind >= 1 && kind <= 9 && (layer < 0 || layer >= c.num_layers))
+  if (((kind >= 1 && kind <= 9) || kind == 12) && (layer < 0 || layer >= c.num_layers))
     return set_error(PO_ERR_ARG, "po_load_weight: layer %d out of range", layer);
   cudaSetDevice(e->device);
   void* dst = nullptr;
   int64_t expect = 0;
   bool norm = false;
-  auto& ly = e->layers[(kind >= 1 && kind <= 9) ? layer : 0];
+  auto& ly = e->layers[((kind >= 1 && kind <= 9) || kind == 12) ? layer : 0];
   switch (kind) {
     case 0: dst = e->embed; expect = (int64_t)c.vocab * h; break;
     case 1: dst = ly.attn_norm; expect = h; norm = true; break;
@@ -363,6 +369,9 @@ int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, 
     case 9: dst = ly.wdown; expect = (int64_t)h * I; break;
     case 10: dst = e->final_norm; expect = h; norm = true; break;
     case 11: dst = e->lm_head; expect = (int64_t)c.vocab * h; break;
+    case 12:
+      if (!c.qkv_bias) return set_error(PO_ERR_ARG, "po_load_weight: model has no qkv bias");
+      dst = ly.bqkv; expect = (int64_t)e->qkv_cols(); norm = true; break;
     default: return set_error(PO_ERR_ARG, "po_load_weight: unknown kind %d", kind);
   }
   if (nelem != expect)
@@ -474,6 +483,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.out = e->qkv + (size_t)n_c * qkvc; g.ldo = qkvc;
     g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
     g.split_ws = e->gemm_ws;
+    g.bias = ly.bqkv;
     mark(KC_QKV, true);
     rc |= po::gemm_launch(e->map_xn, ly.map_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);

@@ -215,6 +215,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tmem_ld32(taddr + h * 128 + half * 32, x1);
             tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
             tmem_ld_wait();
+            if (args.bias) {
+              const float* b1 = args.bias + hcol + half * 32;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                x1[i] = __float_as_uint(__uint_as_float(x1[i]) + b1[i]);
+                x2[i] = __float_as_uint(__uint_as_float(x2[i]) + b1[64 + i]);
+              }
+            }
             if (row < args.M) {
               if (rot) {
 #pragma unroll
@@ -295,11 +303,17 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       }
     } else if constexpr (EPI == EPI_QKV_ROPE) {
       const int head_col = col % 128;
+      if (a.bias) {
+        acc.x += a.bias[col]; acc.y += a.bias[col + 1]; acc.z += a.bias[col + 2]; acc.w += a.bias[col + 3];
+      }
       if (col < a.rope_cols && head_col < 64) {
         float4 x2 = *reinterpret_cast<const float4*>(p + 64);
         for (int s = 1; s < a.k_splits; ++s) {
           const float4 v = *reinterpret_cast<const float4*>(p + 64 + s * slice);
           x2.x += v.x; x2.y += v.y; x2.z += v.z; x2.w += v.w;
+        }
+        if (a.bias) {
+          x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
         }
         const float2* cs = a.rope + (long long)(a.pos_offset + row) * 64 + head_col;
         const float4 x1 = acc;

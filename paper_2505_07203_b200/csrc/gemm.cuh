@@ -22,6 +22,7 @@ struct GemmArgs {
   const float2* rope;   // [pos][64] (cos, sin) for EPI_QKV_ROPE
   int pos_offset;       // absolute position of row 0
   int rope_cols;        // columns [0, rope_cols) are rotated (q and k heads)
+  const float* bias;    // EPI_QKV_ROPE: optional per-column bias added before RoPE (Qwen2 q/k/v bias)
   // split-K (small-M GEMMs, e.g. prefix-hit requests): k_splits > 1 writes fp32 partials to `split_ws`
   // ([k_splits][M][N]) and a reduce kernel applies the epilogue after summing in a fixed order.
   int k_splits;

@@ -54,6 +54,14 @@ __global__ void init_norm_kernel(float* dst, long long n, uint64_t seed, uint32_
   }
 }
 
+__global__ void init_bias_kernel(float* dst, long long n, uint64_t seed, uint32_t tid) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(__float2bfloat16_rn(__fmul_rn(0.1f, unit_uniform(seed, tid, i))));
+}
+void launch_init_bias(float* dst, long long n, uint64_t seed, uint32_t tid, cudaStream_t s) {
+  init_bias_kernel<<<64, 256, 0, s>>>(dst, n, seed, tid);
+}
+
 void launch_init_bf16(__nv_bfloat16* dst, long long rows, long long cols, uint64_t seed, uint32_t tid, uint32_t tid2,
                       float scale, int mode, cudaStream_t s) {
   init_bf16_kernel<<<148 * 8, 256, 0, s>>>(dst, rows, cols, seed, tid, tid2, scale, mode);

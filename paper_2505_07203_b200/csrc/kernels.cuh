@@ -22,6 +22,8 @@ enum InitMode : int {
 void launch_init_bf16(__nv_bfloat16* dst, long long rows, long long cols, uint64_t seed, uint32_t tid, uint32_t tid2,
                       float scale, int mode, cudaStream_t s);
 void launch_init_norm(float* dst, long long n, uint64_t seed, uint32_t tid, cudaStream_t s);
+// dst (fp32) = bf16(0.1 * u): random-init q/k/v bias
+void launch_init_bias(float* dst, long long n, uint64_t seed, uint32_t tid, cudaStream_t s);
 
 // resid[r, :] = float(embed[tokens[r] % vocab, :])
 void launch_embed(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden, float* resid,

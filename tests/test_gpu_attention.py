@@ -52,7 +52,9 @@ def run(n_total, q_offset, hq, hkv, scale=1.0, seed=0):
 
 
 @pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (100, 2, 1), (128, 2, 1), (129, 4, 2), (1000, 8, 2),
-                                      (2048, 2, 1), (3000, 32, 8)])
+                                      (2048, 2, 1), (3000, 32, 8),
+                                      # odd GQA groups (Qwen-2.5-32B is 40/8): query-block-pair CTAs
+                                      (1, 5, 1), (300, 5, 1), (1000, 10, 2), (2600, 40, 8), (129, 3, 3)])
 def test_attention_cold(n, hq, hkv):
     out, ref, err = run(n, 0, hq, hkv, seed=n)
     assert torch.isfinite(out.float()).all()
@@ -61,8 +63,9 @@ def test_attention_cold(n, hq, hkv):
 
 @pytest.mark.parametrize("n,off", [(300, 16), (1000, 992), (2000, 1040), (4096, 4095), (1500, 128),
                                    (20000, 19840), (20000, 19000), (9000, 8850)])
-def test_attention_prefix_offset(n, off):
-    out, ref, err = run(n, off, 8, 2, seed=n + off)
+@pytest.mark.parametrize("hq,hkv", [(8, 2), (10, 2)])
+def test_attention_prefix_offset(n, off, hq, hkv):
+    out, ref, err = run(n, off, hq, hkv, seed=n + off)
     assert torch.isfinite(out.float()).all()
     assert err < TOL, err
 
@@ -74,11 +77,11 @@ def test_attention_large_logits_rescale():
     assert err < TOL, err
 
 
-def test_attention_rejects_odd_group():
-    qkv = torch.zeros(16, 5 * 128, dtype=torch.bfloat16, device="cuda")
+def test_attention_rejects_non_integer_group():
+    qkv = torch.zeros(16, 7 * 128, dtype=torch.bfloat16, device="cuda")
     out = torch.zeros(16, 3 * 128, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(_lib.PrefillOnlyError):
-        _lib.call("po_op_attention", _p(qkv), 5 * 128, 16, 0, 3, 1, _p(out), 3 * 128, None)
+        _lib.call("po_op_attention", _p(qkv), 7 * 128, 16, 0, 3, 2, _p(out), 3 * 128, None)
 
 
 @pytest.mark.parametrize("n,off", [(1, 0), (200, 0), (300, 176), (1000, 512)])

@@ -20,6 +20,9 @@ LOGIT_RTOL = 2e-2
 YES_NO = [9642, 2822]  # build-chosen "Yes"/"No" ids (Llama-3 tokenizer ids), valid in every preset vocab
 
 SMALL = ModelConfig("small", 2, 1024, 8, 2, 128, 2816, 4096)
+# Qwen2-style: odd GQA group (5), q/k/v bias, plain RoPE theta 1e6, eps 1e-6 (Qwen-2.5-32B family at tiny size)
+TINY_QWEN = ModelConfig("tiny-qwen", 2, 1280, 10, 2, 128, 1024, 32000, rms_eps=1e-6, rope_theta=1_000_000.0,
+                        rope_scaling=0, qkv_bias=True)
 
 
 def tokens_for(seed: int, n: int) -> np.ndarray:
@@ -83,6 +86,18 @@ def test_small_gqa_chunked_mlp():
     with Engine(SMALL, seed=7, max_tokens=2048, chunk=512, pool_blocks=64) as e:
         res = e.prefill(toks, [5, 11, 4095])
     check_against_oracle(SMALL, res, toks, [5, 11, 4095], 7)
+
+
+def test_qwen_style_odd_group_and_bias():
+    toks = tokens_for(17, 1300)
+    with Engine(TINY_QWEN, seed=5, max_tokens=2048, chunk=512, pool_blocks=128) as e:
+        res = e.prefill(toks, YES_NO)
+        check_against_oracle(TINY_QWEN, res, toks, YES_NO, 5)
+        # prefix hit through the pool on the query-block-pair attention path
+        slots = list(range(1300 // 16))
+        e.prefill(toks, YES_NO, 0, slots)
+        warm = e.prefill(toks, YES_NO, 1024, slots)
+        check_against_oracle(TINY_QWEN, warm, toks, YES_NO, 5)
 
 
 def test_chunk_size_does_not_change_result():
