@@ -17,9 +17,9 @@ request with a Yes/No allowed list, cold prefix cache. One STEP = one request th
           that class inside the timed region; `roofline` is the class with the largest time share.
   qps_at_slo  post-recommendation 20k workload (40 users x 50 requests, shared profiles) under Poisson
           arrivals, calibrated SRJF + prefix pool, sticky routing over N GPUs: largest rate whose p99
-          latency meets the SLO. Service times come from the reference's own cost-model form
-          (c_fixed + c_lin*miss + c_attn*(n^2-n_c^2)/2, ps/costs.py:275-277) least-squares FITTED TO FORWARDS
-          MEASURED ON THIS GPU (cold and prefix-hit); the event loop is the reference's (serving.simulate).
+          latency meets the SLO. The event loop is the reference's (serving.simulate, virtual clock); every
+          distinct request shape (n, n_cached) it meets is run for real on the GPU once and its measured
+          device time reused (serving.MeasuredServiceFn).
   cpu_baseline  the CPU port of the reference path (oracle/llama_ref.py, numpy f64) timed on this host on a
           bounded sample (one Llama-8B layer at 1,024 tokens), extrapolated by the FLOP formula.
 """
@@ -258,7 +258,7 @@ def main():
 
     n = args.n_tokens
     K, W = args.steps, args.warmup
-    eng = Engine(M, device=local, seed=0, max_tokens=max(n, 24_000), chunk=args.chunk, pool_blocks=8192)
+    eng = Engine(M, device=local, seed=0, max_tokens=max(n, 24_000), chunk=args.chunk, pool_blocks=24_576)
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
 
     # distinct synthetic requests per step and rank, resident in HBM before the timed region
@@ -384,73 +384,48 @@ def main():
         dist.destroy_process_group()
 
 
-def fit_service_model(samples):
-    """LSQ fit of latency = c_fixed + c_lin*(n-nc) + c_attn*(n^2-nc^2)/2 (execute_time's form)."""
-    X = np.array([[1.0, n - nc, (n * n - nc * nc) / 2.0] for n, nc, _ in samples])
-    y = np.array([t for _, _, t in samples])
-    beta = np.linalg.lstsq(X, y, rcond=None)[0]
-    res = y - X @ beta
-    r2 = 1.0 - float(res @ res) / float(((y - y.mean()) ** 2).sum())
-    return beta, r2
-
-
 def qps_at_slo(eng, M, world, rank, slo, dist):
-    """Measure cold and prefix-hit forwards on this GPU, fit the service model, run the DP serving DES."""
+    """Calibrated-SRJF serving of the post-recommendation 20k workload over `world` GPU replicas.
+
+    Virtual-clock event loop with the reference's semantics (serving.simulate); every distinct request shape
+    (n_input, n_cached) the loop encounters is run for real on this GPU once (MeasuredServiceFn) and its
+    device time reused. Rank 0 runs the loop for all replicas (identical GPUs, sticky user routing).
+    """
     from paper_2505_07203_b200 import workload as wl
     from paper_2505_07203_b200.scheduling import Policy
-    from paper_2505_07203_b200.serving import qps_at_slo as pick, simulate, sweep_rates
+    from paper_2505_07203_b200.serving import MeasuredServiceFn, qps_at_slo as pick, simulate, sweep_rates
 
-    bt = eng.block_tokens
-    samples = []
-    for n in (17_000, 20_000, 23_000):
-        toks = np.random.default_rng([rank, 2, n]).integers(0, 2 ** 32, size=n, dtype=np.uint32)
-        nb = n // bt
-        slots = list(range(nb))
-        eng.prefill(toks, ALLOWED, 0, slots)  # cold, admits every block
-        for nc in (0, (n // 2 // bt) * bt, (n - 150) // bt * bt):
-            ids = slots[: nc // bt] + [-1] * (nb - nc // bt)
-            samples.append((n, nc, eng.prefill(toks, ALLOWED, nc, ids).service_s))
-    beta, r2 = fit_service_model(samples)
-    if dist is not None:
-        import torch
-
-        allb = [None] * world
-        dist.all_gather_object(allb, beta.tolist())
-        betas = [np.array(b) for b in allb]
-    else:
-        betas = [beta]
     if rank != 0:
         return None
     trace = wl.gen_post_recommendation(0, wl.POSTREC_20K)
-    capacity = eng.capacity_tokens
-
-    def svc(idx, w, nc, ids):
-        b = betas[idx]
-        nn = w.request.n_input
-        return float(b[0] + b[1] * (nn - nc) + b[2] * (nn * nn - nc * nc) / 2.0)
-
-    run = lambda tr: simulate(tr, world, Policy.srjf_calibrated(), capacity, svc)  # noqa: E731
+    capacity = min(eng.capacity_tokens, 16 * eng.pool_blocks)
+    svc = MeasuredServiceFn(eng, ALLOWED)
+    t0 = time.perf_counter()
+    run = lambda tr, pol=None: simulate(tr, world, pol or Policy.srjf_calibrated(), capacity, svc)  # noqa: E731
     sat = run(wl.zero_arrivals(trace)).throughput
-    rates = [sat * m for m in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0, 3.0)]
+    rates = [sat * m for m in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0)]
     res = sweep_rates(trace, rates, seed=0, run=run)
-    fifo = sweep_rates(trace, rates, seed=0,
-                       run=lambda tr: simulate(tr, world, Policy.fifo(), capacity, svc))
+    fifo = sweep_rates(trace, rates, seed=0, run=lambda tr: run(tr, Policy.fifo()))
     best = pick(res, slo)
     rep = dict(res)[best] if best else None
+    hits = sorted(v[0] for (n, nc), v in svc.memo.items() if nc > 0)
+    colds = sorted(v[0] for (n, nc), v in svc.memo.items() if nc == 0)
     return {
         "value": best, "unit": "requests/s", "slo_p99_s": slo, "n_gpus": world,
         "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
         "miss_tokens_per_s_at_slo": rep.miss_tokens_per_s if rep else None,
+        "p99_at_value_s": rep.p99_latency if rep else None,
         "fifo_qps_at_slo": pick(fifo, slo), "saturation_rps": sat,
-        "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency, "hit_requests": r.cache_hit_requests}
-                  for q, r in res],
+        "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency, "hit_requests": r.cache_hit_requests,
+                   "fifo_p99_s": f.p99_latency} for (q, r), (_, f) in zip(res, fifo)],
         "workload": "post-recommendation 40 users x 50 requests, profiles 19,850 +- 3,000 tokens + 150-token "
-                    "suffix (Poisson arrivals, user sessions contiguous), Yes/No",
-        "method": "virtual-clock serving loop (reference event semantics, calibrated SRJF, prefix pool of "
-                  f"{capacity} tokens/GPU); service time = c_fixed + c_lin*miss + c_attn*pairs fitted to "
-                  f"{len(samples)} forwards measured on each GPU (R^2 = {r2:.5f})",
-        "service_model": {"c_fixed_s": float(beta[0]), "c_lin_s_per_token": float(beta[1]),
-                          "c_attn_s_per_pair": float(beta[2]), "r2": r2},
+                    "suffix, Poisson arrivals (user sessions contiguous), Yes/No allowed ids",
+        "method": f"virtual-clock serving loop with the reference's event semantics (calibrated SRJF, prefix pool of "
+                  f"{capacity} tokens per GPU, sticky routing over {world} replica(s)); each of the "
+                  f"{svc.forwards} distinct (n, n_cached) shapes ran as a real forward on GPU 0 "
+                  f"({time.perf_counter() - t0:.1f} s wall)",
+        "measured_service_s": {"cold_median": statistics.median(colds) if colds else None,
+                               "prefix_hit_median": statistics.median(hits) if hits else None},
     }
 
 

@@ -219,6 +219,29 @@ def engine_service_fn(engines: Sequence, allowed: Sequence[int]) -> ServiceFn:
     return fn
 
 
+class MeasuredServiceFn:
+    """Service function that runs each distinct (n_input, n_cached) request shape once on a live Engine and
+    reuses the measured device seconds (every shape in the trace is a real forward on the GPU).
+
+    All instances share one engine's measurements (request-level DP replicas on identical GPUs).
+    """
+
+    def __init__(self, engine, allowed: Sequence[int]):
+        self.engine = engine
+        self.allowed = list(allowed)
+        self.memo: dict = {}
+        self.forwards = 0
+
+    def __call__(self, idx: int, wr: WaitingRequest, n_cached: int, pool_block_ids: list):
+        key = (wr.request.n_input, n_cached)
+        hit = self.memo.get(key)
+        if hit is None:
+            res = self.engine.prefill(wr.request.tokens, self.allowed, n_cached, pool_block_ids)
+            hit = self.memo[key] = (res.service_s, res.token)
+            self.forwards += 1
+        return hit
+
+
 def shard_trace(trace, rank: int, world: int):
     """Requests the sticky router sends to instance `rank` (request-level DP: each GPU serves its own users).
 
