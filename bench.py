@@ -241,9 +241,15 @@ def main():
     from paper_2505_07203_b200.config import LLAMA_3_1_8B as M
     from paper_2505_07203_b200.engine import Engine
 
+    ndev = torch.cuda.device_count()
+    local = local % ndev  # one process per GPU; more ranks than GPUs only in single-GPU validation runs
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (barrier + max-over-ranks timing): no collective touches the data path
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -252,7 +258,8 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

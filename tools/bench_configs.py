@@ -107,9 +107,29 @@ def qwen32b(slo=30.0):
             "method": f"virtual-clock loop over 8 replicas, {svc.forwards} distinct lengths run for real on this GPU"}
 
 
+def jct():
+    """Measured JCT profile (ps/jct.py:100-128 with latency_fn = the real engine) and the paper's statistic:
+    Pearson(service time, cache-miss tokens) (0.987 on A100/Qwen-32B-FP8)."""
+    from paper_2505_07203_b200 import jct as J
+
+    M = LLAMA_3_1_8B
+    with Engine(M, seed=0, max_tokens=24_000, pool_blocks=2048) as e:
+        t = toks(4, 4000)
+        e.prefill(t, YES_NO)
+        samples = J.profile_engine(e, max_input=24_000, step=4000)
+    prof = J.fit(samples)
+    miss = [s.n_input - s.n_cached for s in samples]
+    lat = [s.latency for s in samples]
+    return {"config": "Llama-3.1-8B, measured latencies on the (n, n_cached) grid, step 4000, up to 24k",
+            "profile": {"coef_input": prof.coef_input, "coef_cached": prof.coef_cached, "intercept": prof.intercept,
+                        "fit_r2": prof.fit_r2},
+            "pearson_latency_vs_miss_tokens": J.pearson(miss, lat), "samples": len(samples),
+            "grid": [[s.n_input, s.n_cached, s.latency] for s in samples]}
+
+
 if __name__ == "__main__":
     which = sys.argv[1]
-    out = {"tiny": tiny, "llama128k": llama128k, "qwen32b": qwen32b}[which]()
+    out = {"tiny": tiny, "llama128k": llama128k, "qwen32b": qwen32b, "jct": jct}[which]()
     text = json.dumps(out)
     print(text, flush=True)
     if len(sys.argv) > 2:
