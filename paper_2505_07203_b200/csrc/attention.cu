@@ -56,9 +56,17 @@ struct AttnArgs {
   int tiles_per_split;
   float* part_o;      // [splits][n_q][hq*128] unnormalised fp32 partial outputs (splits > 1)
   float2* part_ml;    // [splits][n_q][hq] (running max in log2 units, running sum)
-  int qpair;          // 0: the two TMEM slots hold two query heads of one GQA group (even groups)
-                      // 1: they hold two consecutive 128-row query blocks of one head (any group, e.g. 40/8)
+  int mode;           // what the two 128-row TMEM slots of a CTA hold (see AttnLayout)
+  int R;              // MODE_PACKED: query rows per head in a slot (128 / GQA group)
+  int G;              // GQA group size (query heads per kv head)
+  int num_units;      // CTAs per split: query blocks (HEADS x head pairs), block pairs x heads, or chunk pairs x kv
 };
+
+// Slot layouts. HEADS: two query heads of one GQA group over the same 128-row query block (K/V shared).
+// QBLOCKS: two consecutive 128-row query blocks of one head (odd groups, e.g. Qwen 40/8). PACKED: short queries
+// (prefix hits) - each slot stacks the G heads of one kv group over R = 128/G query rows, so a 160-token miss
+// suffix fills 128-row MMA tiles instead of padding every head to 128 rows.
+enum AttnMode : int { MODE_HEADS = 0, MODE_QBLOCKS = 1, MODE_PACKED = 2 };
 
 // ---- packed f32x2 math (sm_100 FFMA2 / FADD2) and a polynomial exp2 on the FMA pipe (MUFU offload)
 __device__ __forceinline__ uint64_t pk2(float a, float b) {
@@ -194,7 +202,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap map, const AttnArgs a) {
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_q,
+                    const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                       // 2 tiles
@@ -213,30 +222,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = warp_id();
   const int lane = lane_id();
 
-  // heaviest (longest causal extent) query blocks first. Slot i of this CTA: head hs_i, first position qs_i.
+  // heaviest (longest causal extent) units first. Slot i of this CTA: head hs_i (first head of the kv group
+  // when packed), first query position qs_i; rows_slot query rows per head in the slot.
+  const int unit = a.num_units - 1 - blockIdx.x / (a.splits * (a.mode == MODE_HEADS ? a.hkv * a.pairs
+                                                                : a.mode == MODE_QBLOCKS ? a.hq : a.hkv));
   int split, g, hs0, hs1, qs0, qs1;
-  if (!a.qpair) {
+  int rows_slot = BQ;
+  if (a.mode == MODE_HEADS) {
     const int per_qb = a.hkv * a.pairs * a.splits;
-    const int qb = a.num_qb - 1 - blockIdx.x / per_qb;
     int rem = blockIdx.x % per_qb;
     split = rem % a.splits;
     rem /= a.splits;
     g = rem / a.pairs;
     hs0 = g * (2 * a.pairs) + 2 * (rem % a.pairs);
     hs1 = hs0 + 1;
-    qs0 = qs1 = a.q_offset + qb * BQ;
-  } else {
-    const int per = a.hq * a.splits;
-    const int qb2 = (a.num_qb + 1) / 2 - 1 - blockIdx.x / per;
-    const int rem = blockIdx.x % per;
+    qs0 = qs1 = a.q_offset + unit * BQ;
+  } else if (a.mode == MODE_QBLOCKS) {
+    const int rem = blockIdx.x % (a.hq * a.splits);
     split = rem % a.splits;
     hs0 = hs1 = rem / a.splits;
-    g = hs0 / (a.hq / a.hkv);
-    qs0 = a.q_offset + qb2 * 2 * BQ;
+    g = hs0 / a.G;
+    qs0 = a.q_offset + unit * 2 * BQ;
     qs1 = qs0 + BQ;
+  } else {
+    const int rem = blockIdx.x % (a.hkv * a.splits);
+    split = rem % a.splits;
+    g = rem / a.splits;
+    hs0 = hs1 = g * a.G;
+    rows_slot = a.R;
+    qs0 = a.q_offset + unit * 2 * a.R;
+    qs1 = qs0 + a.R;
   }
   const int q_lo = qs0;                                     // earliest query position of the CTA
-  const int q_hi = min(qs1 + BQ - 1, a.n_total - 1);        // last real query position of the CTA
+  const int q_hi = min(qs1 + rows_slot - 1, a.n_total - 1); // last real query position of the CTA
   const int all_tiles = q_hi / BKV + 1;
   const int t0 = split * a.tiles_per_split;                 // this CTA's KV tile range [t0, t0 + n_tiles)
   const int n_tiles = max(0, min(all_tiles, t0 + a.tiles_per_split) - t0);
@@ -258,12 +276,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       const uint64_t keep = l2_policy_evict_last();
       mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
+      if (a.mode != MODE_PACKED) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int half = 0; half < 2; ++half)
-          tma_load_2d(sQ + i * TILE_BYTES + half * BOX_BYTES, &map, q_full, (i ? hs1 : hs0) * HD + half * 64,
-                      i ? qs1 : qs0);
+          for (int half = 0; half < 2; ++half)
+            tma_load_2d(sQ + i * TILE_BYTES + half * BOX_BYTES, &map, q_full, (i ? hs1 : hs0) * HD + half * 64,
+                        i ? qs1 : qs0);
+      } else {
+        // slot i = G stacked (R rows x 128) head tiles; each R-row box lands 1024-B aligned (R % 8 == 0)
+        for (int i = 0; i < 2; ++i)
+          for (int k = 0; k < a.G; ++k)
+#pragma unroll
+            for (int half = 0; half < 2; ++half)
+              tma_load_2d(sQ + i * TILE_BYTES + half * BOX_BYTES + k * a.R * 128, &map_q, q_full,
+                          (g * a.G + k) * HD + half * 64, i ? qs1 : qs0);
+      }
       const int kcol = a.hq * HD + g * HD;
       const int vcol = (a.hq + a.hkv) * HD + g * HD;
       for (int j = 0; j < n_tiles; ++j) {
@@ -336,9 +364,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + i * 128;
     const uint32_t o_addr = tmem + lane_base + 256 + i * 128;
-    const int my_qlo = i ? qs1 : qs0;
-    const int my_h = i ? hs1 : hs0;
-    const int pos = my_qlo + r;
+    const int my_qlo = i ? qs1 : qs0;  // smallest query position in the slot
+    const bool packed = a.mode == MODE_PACKED;
+    const int my_h = packed ? (i ? hs1 : hs0) + r / a.R : (i ? hs1 : hs0);
+    const int qr = packed ? r % a.R : r;  // query row within the slot
+    const int pos = my_qlo + qr;
     float m = -INFINITY;  // running max (scaled, log2 units), possibly stale
     float l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
@@ -357,7 +387,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     mbar_wait(&o_final[i], 0);
     tc_fence_after();
-    const int row = my_qlo - a.q_offset + r;
+    const int row = (packed && qr >= rows_slot) ? a.n_q : my_qlo - a.q_offset + qr;
     if (a.splits == 1) {
       const float inv = 1.0f / l;
       __nv_bfloat16* dst = a.out + (long long)row * a.ldo + my_h * HD;
@@ -407,7 +437,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 // out[row, h, :] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s over the KV splits that exist for the row's block
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml, int n_q,
-                                    int hq, int splits, int tiles_per_split, int q_offset, int n_total, int qpair,
+                                    int hq, int splits, int tiles_per_split, int q_offset, int n_total, int span,
                                     __nv_bfloat16* __restrict__ out, long long ldo) {
   const long long total = (long long)n_q * hq * (HD / 4);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -416,7 +446,6 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o, const floa
     const long long rh = i / (HD / 4);
     const int h = static_cast<int>(rh % hq);
     const int row = static_cast<int>(rh / hq);
-    const int span = qpair ? 2 * BQ : BQ;  // query rows per CTA
     const int q_hi = min(q_offset + (row / span) * span + span - 1, n_total - 1);
     const int all_tiles = q_hi / BKV + 1;
     const int ns = min(splits, (all_tiles + tiles_per_split - 1) / tiles_per_split);
@@ -440,12 +469,45 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o, const floa
   }
 }
 
-// KV splits for a launch: split only when the (query block x head pair) grid cannot fill the SMs.
-void attention_split_plan(int n_total, int q_offset, int hq, int hkv, int* splits, int* tiles_per_split) {
+struct AttnLayout {
+  int mode, R, G, units, ctas, span;  // units = CTAs per KV split; span = query rows per CTA
+};
+
+AttnLayout attention_layout(int n_total, int q_offset, int hq, int hkv) {
+  AttnLayout L{};
   const int n_q = n_total - q_offset;
   const int num_qb = (n_q + BQ - 1) / BQ;
-  const bool qpair = (hq / hkv) % 2 != 0;
-  const int base = qpair ? ((num_qb + 1) / 2) * hq : num_qb * hkv * (hq / hkv / 2);
+  L.G = hq / hkv;
+  if (L.G % 2) {
+    L.mode = MODE_QBLOCKS;
+    L.units = (num_qb + 1) / 2;
+    L.ctas = L.units * hq;
+    L.span = 2 * BQ;
+  } else {
+    L.mode = MODE_HEADS;
+    L.units = num_qb;
+    L.ctas = num_qb * hq / 2;
+    L.span = BQ;
+  }
+  L.R = BQ;
+  // short queries (prefix hits): stack the group's heads into the 128-row tiles when that shrinks the grid
+  if (L.G > 1 && BQ % L.G == 0 && (BQ / L.G) % 8 == 0 && L.ctas < 148) {
+    const int R = BQ / L.G;
+    const int pairs = ((n_q + R - 1) / R + 1) / 2;
+    if (pairs * hkv < L.ctas) {
+      L.mode = MODE_PACKED;
+      L.R = R;
+      L.units = pairs;
+      L.ctas = pairs * hkv;
+      L.span = 2 * R;
+    }
+  }
+  return L;
+}
+
+// KV splits for a launch: split only when the layout's grid cannot fill the SMs.
+void attention_split_plan(int n_total, int q_offset, int hq, int hkv, int* splits, int* tiles_per_split) {
+  const int base = attention_layout(n_total, q_offset, hq, hkv).ctas;
   const int max_tiles = (n_total - 1) / BKV + 1;
   int s = 1;
   if (base < 148 && max_tiles >= 8) {
@@ -470,8 +532,10 @@ size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv) {
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
                   cudaStream_t stream, void* workspace, size_t workspace_bytes) {
   if (hq % hkv) return -3;
-  CUtensorMap map;
+  const AttnLayout lay = attention_layout(n_total, q_offset, hq, hkv);
+  CUtensorMap map, map_q;
   if (make_tmap_2d_bf16(&map, qkv, ld, n_total, ld * 2, 64, 128)) return -2;
+  if (make_tmap_2d_bf16(&map_q, qkv, ld, n_total, ld * 2, 64, lay.R)) return -2;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -483,8 +547,11 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
   a.n_q = n_total - q_offset;
   a.hq = hq;
   a.hkv = hkv;
-  a.qpair = (hq / hkv) % 2 != 0;
-  a.pairs = a.qpair ? 1 : hq / hkv / 2;
+  a.mode = lay.mode;
+  a.R = lay.R;
+  a.G = lay.G;
+  a.num_units = lay.units;
+  a.pairs = lay.G % 2 ? 1 : lay.G / 2;
   a.num_qb = (a.n_q + BQ - 1) / BQ;
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
@@ -500,13 +567,13 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
     a.part_ml = reinterpret_cast<float2*>(static_cast<char*>(workspace) +
                                           (size_t)a.splits * a.n_q * hq * HD * sizeof(float));
   }
-  const int grid = (a.qpair ? ((a.num_qb + 1) / 2) * hq : a.num_qb * hkv * a.pairs) * a.splits;
-  attn_fwd_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(map, a);
+  const int grid = lay.ctas * a.splits;
+  attn_fwd_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(map, map_q, a);
   if (a.splits > 1) {
     const long long total = (long long)a.n_q * hq * (HD / 4);
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
     attn_combine_kernel<<<blocks, 256, 0, stream>>>(a.part_o, a.part_ml, a.n_q, hq, a.splits, a.tiles_per_split,
-                                                    q_offset, n_total, a.qpair, a.out, ldo);
+                                                    q_offset, n_total, lay.span, a.out, ldo);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
