@@ -43,7 +43,8 @@ struct po_engine {
     __nv_bfloat16 *wqkv, *wo, *wgu, *wdown;
     float *attn_norm, *mlp_norm;
     float* bqkv = nullptr;  // q/k/v bias (qkv_bias models), fp32 holding bf16 values
-    CUtensorMap map_qkv, map_o, map_gu, map_down;
+    CUtensorMap map_qkv, map_o, map_gu, map_down;      // 256-row boxes (1-CTA kernel)
+    CUtensorMap map2_qkv, map2_o, map2_gu, map2_down;  // 128-row boxes (2-CTA pair kernel)
   };
   std::vector<Layer> layers;
   // arena
@@ -234,7 +235,9 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     }
     po::launch_init_norm(ly.mlp_norm, h, seed, layer_tid(l, K_MLP_NORM), s);
     if (po::make_tmap_b(&ly.map_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b(&ly.map_o, ly.wo, ctxc, h, ctxc) ||
-        po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I))
+        po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I) ||
+        po::make_tmap_a(&ly.map2_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_a(&ly.map2_o, ly.wo, ctxc, h, ctxc) ||
+        po::make_tmap_a(&ly.map2_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_a(&ly.map2_down, ly.wdown, I, h, I))
       return fail(PO_ERR_CUDA, "weight tensor-map encode failed");
   }
 
@@ -427,6 +430,12 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
   return n_c;
 }
 
+// 2-CTA pair GEMM for M > 128 (256-row pair tiles), 1-CTA 128-row tiles below
+int gemm(const CUtensorMap& a, const CUtensorMap& b1, const CUtensorMap& b2, int epi, const po::GemmArgs& g,
+         cudaStream_t s) {
+  return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(a, b2, epi, g, s) : po::gemm_launch(a, b1, epi, g, s);
+}
+
 enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
               KC_COUNT };
 
@@ -485,7 +494,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.split_ws = e->gemm_ws;
     g.bias = ly.bqkv;
     mark(KC_QKV, true);
-    rc |= po::gemm_launch(e->map_xn, ly.map_qkv, po::EPI_QKV_ROPE, g, s);
+    rc |= gemm(e->map_xn, ly.map_qkv, ly.map2_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
     ++launches;
     if (n_admit) {
@@ -509,7 +518,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     go.M = rows; go.N = h; go.K = ctxc;
     go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
     mark(KC_O, true);
-    rc |= po::gemm_launch(e->map_ctx, ly.map_o, po::EPI_RESID_F32, go, s);
+    rc |= gemm(e->map_ctx, ly.map_o, ly.map2_o, po::EPI_RESID_F32, go, s);
     mark(KC_O, false);
     ++launches;
     for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
@@ -521,13 +530,13 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
       mark(KC_GATE_UP, true);
-      rc |= po::gemm_launch(e->map_xn, ly.map_gu, po::EPI_SILU_MUL, gu, s);
+      rc |= gemm(e->map_xn, ly.map_gu, ly.map2_gu, po::EPI_SILU_MUL, gu, s);
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
       mark(KC_DOWN, true);
-      rc |= po::gemm_launch(e->map_act, ly.map_down, po::EPI_RESID_F32, gd, s);
+      rc |= gemm(e->map_act, ly.map_down, ly.map2_down, po::EPI_RESID_F32, gd, s);
       mark(KC_DOWN, false);
       launches += 3;
     }

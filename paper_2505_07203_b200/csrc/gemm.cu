@@ -9,6 +9,7 @@
 #include "gemm.cuh"
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 
 namespace po {
 
@@ -81,6 +82,69 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int c
         w[e] = pack_bf16(x0, x1);
       }
       dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// Epilogue of one 128-row x 256-column accumulator (this thread: TMEM lane = output row `row`).
+template <int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t taddr, int row, int nb, int ksp, int t) {
+  if (ksp > 1) {
+    // split-K partial: raw fp32 tile into the workspace slice of this split
+    GemmArgs pa = args;
+    pa.out = args.split_ws + (size_t)(t % ksp) * args.M * args.N;
+    pa.ldo = args.N;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (row < args.M) epilogue_chunk<EPI_F32>(pa, row, nb * BN + c, r);
+    }
+  } else if constexpr (EPI == EPI_QKV_ROPE) {
+    // two 128-column heads per tile; rotate-half pairs (i, i+64)
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int hcol = nb * BN + h * 128;
+      const bool rot = hcol < args.rope_cols;
+      const float2* cs = args.rope + (long long)(args.pos_offset + row) * 64;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        uint32_t x1[32], x2[32];
+        tmem_ld32(taddr + h * 128 + half * 32, x1);
+        tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
+        tmem_ld_wait();
+        if (args.bias) {
+          const float* b1 = args.bias + hcol + half * 32;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            x1[i] = __float_as_uint(__uint_as_float(x1[i]) + b1[i]);
+            x2[i] = __float_as_uint(__uint_as_float(x2[i]) + b1[64 + i]);
+          }
+        }
+        if (row < args.M) {
+          if (rot) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float2 c = cs[half * 32 + i];
+              const float a0 = __uint_as_float(x1[i]);
+              const float b0 = __uint_as_float(x2[i]);
+              x1[i] = __float_as_uint(a0 * c.x - b0 * c.y);
+              x2[i] = __float_as_uint(b0 * c.x + a0 * c.y);
+            }
+          }
+          epilogue_chunk<EPI_BF16>(args, row, hcol + half * 32, x1);
+          epilogue_chunk<EPI_BF16>(args, row, hcol + 64 + half * 32, x2);
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BN + c, r);
     }
   }
 }
@@ -190,64 +254,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row = mb * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      if (ksp > 1) {
-        // split-K partial: raw fp32 tile into the workspace slice of this split
-        GemmArgs pa = args;
-        pa.out = args.split_ws + (size_t)(t % ksp) * args.M * args.N;
-        pa.ldo = args.N;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_ld_wait();
-          if (row < args.M) epilogue_chunk<EPI_F32>(pa, row, nb * BN + c, r);
-        }
-      } else if constexpr (EPI == EPI_QKV_ROPE) {
-        // two 128-column heads per tile; rotate-half pairs (i, i+64)
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int hcol = nb * BN + h * 128;
-          const bool rot = hcol < args.rope_cols;
-          const float2* cs = args.rope + (long long)(args.pos_offset + row) * 64;
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            uint32_t x1[32], x2[32];
-            tmem_ld32(taddr + h * 128 + half * 32, x1);
-            tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
-            tmem_ld_wait();
-            if (args.bias) {
-              const float* b1 = args.bias + hcol + half * 32;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                x1[i] = __float_as_uint(__uint_as_float(x1[i]) + b1[i]);
-                x2[i] = __float_as_uint(__uint_as_float(x2[i]) + b1[64 + i]);
-              }
-            }
-            if (row < args.M) {
-              if (rot) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const float2 c = cs[half * 32 + i];
-                  const float a0 = __uint_as_float(x1[i]);
-                  const float b0 = __uint_as_float(x2[i]);
-                  x1[i] = __float_as_uint(a0 * c.x - b0 * c.y);
-                  x2[i] = __float_as_uint(b0 * c.x + a0 * c.y);
-                }
-              }
-              epilogue_chunk<EPI_BF16>(args, row, hcol + half * 32, x1);
-              epilogue_chunk<EPI_BF16>(args, row, hcol + 64 + half * 32, x2);
-            }
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_ld_wait();
-          if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BN + c, r);
-        }
-      }
+      epilogue_tile<EPI>(args, taddr, row, nb, ksp, t);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
     }
@@ -258,6 +265,146 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+}
+
+
+// ------------------------------------------------------------------ 2-CTA (cta_group::2) variant
+// A CTA pair computes a 256 x 256 tile: each CTA loads its own 128 rows of A and 128 of the 256 B rows (the
+// pair's MMA reads both CTAs' shared memory), so per-CTA B traffic halves vs the 1-CTA 128 x 256 tile. The
+// leader CTA (rank 0) issues tcgen05.mma.cta_group::2 (M256 N256 K16); both CTAs' TMA loads complete on the
+// leader's full barrier; MMA commits multicast to both CTAs' empty / tmem-full barriers; each CTA drains its
+// own 128 accumulator rows and reports to the leader's tmem-empty barrier.
+namespace {
+constexpr int STAGES2 = 6;
+constexpr int HALF_BYTES = 128 * BK * 2;             // 16 KB: 128 rows x 64 bf16
+constexpr int STAGE2_BYTES = 2 * HALF_BYTES;         // A half + B half per CTA
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+}  // namespace
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * HALF_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES2;
+  uint64_t* tfull_bar = empty_bar + STAGES2;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int num_m = (args.M + 2 * BM - 1) / (2 * BM);
+  const int num_n = args.N / BN;
+  const int ksp = args.k_splits > 1 ? args.k_splits : 1;
+  const int num_tiles = num_m * num_n * ksp;
+  const int nk_total = args.K / BK;
+  const int kbps = ksp > 1 ? args.kb_per_split : nk_total;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2);  // one arrival per CTA of the pair (leader's copy is the one used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive / TMA completion
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);  // leader's full_bar[0]
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < num_tiles; t += npairs) {
+        int mb, nb;
+        tile_coords(t / ksp, num_m, num_n, mb, nb);
+        const int kb0 = (t % ksp) * kbps;
+        const int nk = min(nk_total, kb0 + kbps) - kb0;
+        for (int k = 0; k < nk; ++k) {
+          const int kb = kb0 + k;
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * STAGE2_BYTES);
+          const uint32_t fb = full0 + s * 8;
+          tma_load_2d_pair(sA + s * HALF_BYTES, &map_a, fb, kb * BK, args.a_row0 + mb * 2 * BM + rank * BM);
+          tma_load_2d_pair(sB + s * HALF_BYTES, &map_b, fb, kb * BK, nb * BN + rank * (BN / 2));
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int t = pair; t < num_tiles; t += npairs, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_ph = (it >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int kb0 = (t % ksp) * kbps;
+        const int nk = min(nk_total, kb0 + kbps) - kb0;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint64_t adesc = sdesc_kmajor_sw128(smem_u32(sA + s * HALF_BYTES));
+          const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sB + s * HALF_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          mma_commit_pair(&empty_bar[s], 0x3);
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+        mma_commit_pair(&tfull_bar[acc], 0x3);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wq = warp & 3;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    int it = 0;
+    for (int t = pair; t < num_tiles; t += npairs, ++it) {
+      int mb, nb;
+      tile_coords(t / ksp, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_ph = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const int row = mb * 2 * BM + rank * BM + wq * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+      epilogue_tile<EPI>(args, taddr, row, nb, ksp, t);
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 128) mbar_arrive_cluster(tempty0 + acc * 8);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
   }
 }
 
@@ -385,6 +532,7 @@ int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long 
   plan->K = K;
   if (make_tmap_2d_bf16(&plan->map_a, A, K, M, lda * 2, BK, BM)) return -2;
   if (make_tmap_2d_bf16(&plan->map_b, B, K, N, ldb * 2, BK, BN)) return -2;
+  if (make_tmap_2d_bf16(&plan->map_b2, B, K, N, ldb * 2, BK, BM)) return -2;
   return 0;
 }
 
@@ -404,7 +552,55 @@ static void split_plan(int M, int N, int K, int* splits, int* kbps) {
 size_t gemm_split_ws_bytes(int M, int N, int K) {
   int s, kbps;
   split_plan(M, N, K, &s, &kbps);
-  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
+  // pair kernel (M > 128): splits bounded by SM pairs / pair tiles
+  const int tiles_mn = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  const int nk = K / BK;
+  int s2 = 1;
+  if (tiles_mn * 2 <= num_sms() / 2 && nk >= 16) {
+    s2 = (num_sms() / 2) / tiles_mn;
+    s2 = s2 < nk / 8 ? s2 : nk / 8;
+    s2 = s2 > 1 ? s2 : 1;
+  }
+  const int smax = s > s2 ? s : s2;
+  return smax > 1 ? (size_t)smax * M * N * sizeof(float) : 0;
+}
+
+template <int EPI>
+static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, const GemmArgs& in,
+                       cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+    configured = true;
+  }
+  GemmArgs args = in;
+  args.k_splits = 1;
+  const int tiles_mn = ((args.M + 2 * BM - 1) / (2 * BM)) * (args.N / BN);
+  if (args.split_ws) {
+    // pair tiles: split K while fewer than SM-pairs/2 tiles exist (small-M prefix-hit GEMMs)
+    const int nk = args.K / BK;
+    int s = 1;
+    const int pairs = num_sms() / 2;
+    if (tiles_mn * 2 <= pairs && nk >= 16) {
+      s = pairs / tiles_mn;
+      s = s < nk / 8 ? s : nk / 8;
+      s = s > 1 ? s : 1;
+    }
+    if (s > 1) {
+      args.k_splits = s;
+      args.kb_per_split = (nk + s - 1) / s;
+      args.k_splits = (nk + args.kb_per_split - 1) / args.kb_per_split;
+    }
+  }
+  const int tiles = tiles_mn * args.k_splits;
+  const int npairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  gemm2_kernel<EPI><<<2 * npairs, NUM_THREADS, SMEM2_BYTES, stream>>>(map_a, map_b2, args);
+  if (args.k_splits > 1) {
+    const long long total = (long long)args.M * (args.N / 4);
+    const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+    splitk_reduce_kernel<EPI><<<blocks, 256, 0, stream>>>(args);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
 template <int EPI>
@@ -435,6 +631,20 @@ static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const Gemm
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
+int gemm_launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, int epi, const GemmArgs& args,
+                     cudaStream_t stream) {
+  if (args.M <= 0) return 0;
+  if (args.N % BN || args.K % BK) return -3;
+  switch (epi) {
+    case EPI_BF16: return launch_pair<EPI_BF16>(map_a, map_b2, args, stream);
+    case EPI_RESID_F32: return launch_pair<EPI_RESID_F32>(map_a, map_b2, args, stream);
+    case EPI_SILU_MUL: return launch_pair<EPI_SILU_MUL>(map_a, map_b2, args, stream);
+    case EPI_QKV_ROPE: return launch_pair<EPI_QKV_ROPE>(map_a, map_b2, args, stream);
+    case EPI_F32: return launch_pair<EPI_F32>(map_a, map_b2, args, stream);
+    default: return -3;
+  }
+}
+
 int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, const GemmArgs& args,
                 cudaStream_t stream) {
   if (args.M <= 0) return 0;
@@ -449,11 +659,21 @@ int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, con
   }
 }
 
+bool gemm_use_pair(int M) {
+  static int force_1cta = -1;
+  if (force_1cta < 0) {
+    const char* v = getenv("PO_GEMM_1CTA");
+    force_1cta = (v && v[0] == '1') ? 1 : 0;
+  }
+  return !force_1cta && M > BM;
+}
+
 int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t stream) {
   GemmArgs args = in;
   args.M = plan.M;
   args.N = plan.N;
   args.K = plan.K;
+  if (gemm_use_pair(args.M)) return gemm_launch_pair(plan.map_a, plan.map_b2, epi, args, stream);
   return gemm_launch(plan.map_a, plan.map_b, epi, args, stream);
 }
 
