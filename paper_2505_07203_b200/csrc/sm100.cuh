@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 namespace po {
 
@@ -51,11 +52,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef PO_DEBUG_HANG
+__device__ __noinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  long long spins = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    ++spins;
+    if (spins == (1ll << 22) && (threadIdx.x & 31) == 0)
+      printf("HANG block %d thread %d bar_smem 0x%x parity %u\n", blockIdx.x, threadIdx.x, addr, parity);
+    if (spins == (1ll << 27)) __trap();
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   while (!mbar_try_wait(addr, parity)) {
   }
 }
+#endif
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
