@@ -125,7 +125,7 @@ int po_last_service_ms(po_engine* e, float* ms);
 int po_pool_evict(po_engine* e, const int32_t* slots, int32_t n);
 
 /* Engine facts: [0] pool_blocks, [1] weight bytes, [2] arena bytes, [3] pool bytes, [4] bytes per pool block,
- * [5] max_tokens, [6] device free bytes after init. */
+ * [5] max_tokens, [6] device free bytes after init, [7] split-KV / split-K workspace bytes. */
 int po_engine_info(po_engine* e, int64_t* out, int32_t n);
 
 /* Overwrite one weight tensor from host memory (logical, un-interleaved layout; bf16 except norms = fp32).

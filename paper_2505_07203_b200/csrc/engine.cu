@@ -77,7 +77,7 @@ struct po_engine {
   // prefix pool [slot][layer][block_tokens][kv_dim]
   __nv_bfloat16* pool = nullptr;
   int64_t pool_blocks = 0;
-  int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0;
+  int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
   float last_ms = 0.f;
   int last_launches = 0;
@@ -257,7 +257,8 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     for (int nq = 1; nq <= 148 * 128 && nq <= T; nq += 64)
       ws = std::max(ws, po::attention_workspace_bytes((int)T, (int)T - nq, c.n_heads, c.n_kv_heads));
     e->attn_ws_bytes = ws;
-    if (ws && dalloc(e, &e->attn_ws, ws, &e->arena_bytes)) return fail(PO_ERR_CUDA, "attention workspace failed");
+    if (ws && dalloc(e, &e->attn_ws, ws, &e->workspace_bytes))
+      return fail(PO_ERR_CUDA, "attention workspace failed");
     // split-K workspace: largest need over the layer GEMM shapes for every M that triggers splitting
     size_t gw = 0;
     for (int m = 1; m <= 148 * 128 && m <= T; m += 16) {
@@ -267,7 +268,7 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       gw = std::max(gw, po::gemm_split_ws_bytes(m, h, I));
     }
     e->gemm_ws_bytes = gw;
-    if (gw && dalloc(e, &e->gemm_ws, gw, &e->arena_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
+    if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
   }
   const long long max_blocks = T / c.block_tokens + 1;
   if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
@@ -326,9 +327,9 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
 
 int po_engine_info(po_engine* e, int64_t* out, int32_t n) {
   if (!e || !out) return set_error(PO_ERR_ARG, "po_engine_info: null argument");
-  const int64_t v[7] = {e->pool_blocks, e->weight_bytes, e->arena_bytes, e->pool_bytes, e->block_bytes(),
-                        e->cfg.max_tokens, e->free_after};
-  for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
+  const int64_t v[8] = {e->pool_blocks, e->weight_bytes, e->arena_bytes, e->pool_bytes, e->block_bytes(),
+                        e->cfg.max_tokens, e->free_after, e->workspace_bytes};
+  for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
   return PO_OK;
 }
 

@@ -71,14 +71,15 @@ class Engine:
         except _lib.PrefillOnlyError as err:
             _raise(err)
         self._h = handle
-        info = (ctypes.c_int64 * 7)()
-        _lib.check(lib.po_engine_info(self._h, ctypes.addressof(info), 7))
+        info = (ctypes.c_int64 * 8)()
+        _lib.check(lib.po_engine_info(self._h, ctypes.addressof(info), 8))
         self.pool_blocks = int(info[0])
         self.weight_bytes = int(info[1])
         self.arena_bytes = int(info[2])
         self.pool_bytes = int(info[3])
         self.block_bytes = int(info[4])
         self.free_bytes_after_init = int(info[6])
+        self.workspace_bytes = int(info[7])
 
     # ------------------------------------------------------------------ lifecycle
     def close(self):

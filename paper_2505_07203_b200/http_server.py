@@ -1,0 +1,106 @@
+"""HTTP front end for prefill-only requests (the paper's OpenAI-style entry point,
+PAPER.md:403-409). The reference has no server; this is a thin FastAPI layer over serving.Server.submit.
+
+  POST /v1/prefill   {"user_id": 7, "tokens": [...]  or  "prompt": "...", "allowed": [9642, 2822]}
+               ->    {"token": 9642, "index": 0, "probs": [...], "logits": [...], "n_cached": 19840,
+                      "latency_s": 0.013, "service_s": 0.012}
+  GET  /v1/stats     served requests, mean / p99 latency, prefix-hit counts (RequestRecord fields)
+
+No tokenizer assets are available offline: "prompt" text is encoded as its UTF-8 bytes (token id = byte),
+which is enough for prefix sharing to behave like real prompts; pass "tokens" for real tokenizer ids.
+
+  python -m paper_2505_07203_b200.http_server --gpus 1 --model llama-3.1-8b --port 8000
+"""
+
+from __future__ import annotations
+
+import argparse
+import itertools
+import threading
+import time
+
+import numpy as np
+
+
+class _HttpRequest:
+    """Request duck type for the scheduler: .id, .user_id, .n_input, .tokens (pkg/tests/test_scheduler.py:15-20)."""
+
+    __slots__ = ("id", "user_id", "tokens", "n_input")
+
+    def __init__(self, rid: int, user_id: int, tokens: np.ndarray):
+        self.id = rid
+        self.user_id = user_id
+        self.tokens = tokens
+        self.n_input = int(tokens.shape[0])
+
+
+try:  # pydantic / fastapi are optional at import time (the engine does not need them)
+    from pydantic import BaseModel
+
+    class PrefillBody(BaseModel):
+        user_id: int = 0
+        tokens: list[int] | None = None
+        prompt: str | None = None
+        allowed: list[int]
+except ImportError:  # pragma: no cover
+    PrefillBody = None
+
+
+def create_app(server):
+    from fastapi import FastAPI, HTTPException
+
+    app = FastAPI(title="prefillonly-b200")
+    ids = itertools.count()
+    lock = threading.Lock()
+
+    @app.post("/v1/prefill")
+    def prefill(body: PrefillBody):
+        if body.tokens is None and body.prompt is None:
+            raise HTTPException(400, "need tokens or prompt")
+        if not body.allowed:
+            raise HTTPException(400, "allowed must be non-empty")
+        toks = np.asarray(body.tokens if body.tokens is not None else list(body.prompt.encode("utf-8")),
+                          dtype=np.uint32)
+        if toks.size == 0:
+            raise HTTPException(400, "empty prompt")
+        with lock:
+            rid = next(ids)
+        t0 = time.perf_counter()
+        try:
+            res = server.submit(_HttpRequest(rid, body.user_id, toks), body.allowed).result()
+        except ValueError as err:  # CapacityError / ConfigError
+            raise HTTPException(413 if "exceeds" in str(err) else 400, str(err)) from None
+        return {"id": rid, "token": res.token, "index": res.index, "probs": res.probs.tolist(),
+                "logits": res.logits.tolist(), "n_cached": res.n_cached,
+                "latency_s": time.perf_counter() - t0, "service_s": res.service_s}
+
+    @app.get("/v1/stats")
+    def stats():
+        rep = server.report()
+        return {"served": rep.served, "mean_latency_s": rep.mean_latency, "p99_latency_s": rep.p99_latency,
+                "cache_hit_requests": rep.cache_hit_requests, "cache_hit_tokens": rep.cache_hit_tokens}
+
+    return app
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--model", default="llama-3.1-8b")
+    ap.add_argument("--max-tokens", type=int, default=32768)
+    ap.add_argument("--host", default="127.0.0.1")
+    ap.add_argument("--port", type=int, default=8000)
+    args = ap.parse_args()
+    import uvicorn
+
+    from .engine import Engine
+    from .scheduling import Policy
+    from .serving import Server
+
+    engines = [Engine(args.model, device=d, max_tokens=args.max_tokens) for d in range(args.gpus)]
+    srv = Server(engines, Policy.srjf_calibrated())
+    uvicorn.run(create_app(srv), host=args.host, port=args.port)
+
+
+if __name__ == "__main__":
+    main()

@@ -155,3 +155,16 @@ def test_last_row_only_equals_full_last_layer():
 def test_capacity_error(tiny_engine):
     with pytest.raises(CapacityError):
         tiny_engine.prefill(tokens_for(0, 4097), YES_NO)
+
+
+def test_arena_matches_geometry_model():
+    """The engine's allocation is the hybrid-mode peak the geometry module predicts (the profile run)."""
+    from paper_2505_07203_b200 import geometry
+    from paper_2505_07203_b200.config import LLAMA_3_1_8B
+
+    for model, T, chunk in ((TINY, 4096, 1024), (SMALL, 2048, 512), (LLAMA_3_1_8B, 24_000, 8192)):
+        with Engine(model, seed=0, max_tokens=T, chunk=chunk, pool_blocks=4) as e:
+            assert e.arena_bytes == geometry.arena_bytes(model, T, chunk)
+            norms_fp32_extra = (2 * model.num_layers + 1) * model.hidden * 2  # norms held as fp32 on device
+            assert e.weight_bytes == model.weight_bytes + norms_fp32_extra
+            assert e.block_bytes == model.kv_bytes_per_token[1] * 16

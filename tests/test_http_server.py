@@ -1,0 +1,31 @@
+"""HTTP front end over Server.submit, with the CPU stand-in engine of tests/test_server.py."""
+
+import pytest
+
+from test_server import FakeEngine
+
+fastapi = pytest.importorskip("fastapi")
+from fastapi.testclient import TestClient  # noqa: E402
+
+from paper_2505_07203_b200.http_server import create_app  # noqa: E402
+from paper_2505_07203_b200.scheduling import Policy  # noqa: E402
+from paper_2505_07203_b200.serving import Server  # noqa: E402
+
+
+def test_prefill_endpoint_and_prefix_reuse():
+    srv = Server([FakeEngine()], Policy.srjf_calibrated())
+    try:
+        client = TestClient(create_app(srv))
+        profile = "user profile " * 200
+        r1 = client.post("/v1/prefill", json={"user_id": 1, "prompt": profile + "post A", "allowed": [9642, 2822]})
+        assert r1.status_code == 200 and r1.json()["n_cached"] == 0
+        r2 = client.post("/v1/prefill", json={"user_id": 1, "prompt": profile + "post B", "allowed": [9642, 2822]})
+        body = r2.json()
+        assert body["token"] in (9642, 2822) and body["n_cached"] >= 2048
+        r3 = client.post("/v1/prefill", json={"user_id": 2, "tokens": list(range(300)), "allowed": [5]})
+        assert r3.status_code == 200
+        assert client.post("/v1/prefill", json={"user_id": 2, "allowed": [5]}).status_code == 400
+        stats = client.get("/v1/stats").json()
+        assert stats["served"] == 3 and stats["cache_hit_requests"] == 1
+    finally:
+        srv.close()
