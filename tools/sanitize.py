@@ -1,0 +1,32 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import ctypes, sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from paper_2505_07203_b200 import _lib
+from paper_2505_07203_b200.config import TINY
+from paper_2505_07203_b200.engine import Engine
+
+p = lambda t: ctypes.c_void_p(t.data_ptr())
+# GEMM: 1-CTA (M<=128), pair (M>128), split-K, every epilogue
+for M, N, K in ((100, 256, 256), (300, 512, 256), (160, 512, 2048)):
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    resid = torch.zeros(M, N, device="cuda")
+    for epi in (0, 1, 2):
+        _lib.call("po_op_gemm", p(A), K, p(B), K, p(out), N, p(resid), N, M, N, K, epi, None, 0, 0, None)
+# attention: cold, prefix offset (split-KV + packed), odd group
+for n, off, hq, hkv in ((300, 0, 4, 2), (600, 560, 8, 2), (300, 0, 5, 1)):
+    ld = (hq + 2 * hkv) * 128
+    qkv = torch.randn(n, ld, device="cuda").to(torch.bfloat16)
+    out = torch.empty(n - off, hq * 128, dtype=torch.bfloat16, device="cuda")
+    _lib.call("po_op_attention", p(qkv), ld, n, off, hq, hkv, p(out), hq * 128, None)
+# engine: cold, admission, prefix hit
+with Engine(TINY, seed=1, max_tokens=1024, chunk=256, pool_blocks=64) as e:
+    t = np.random.default_rng(0).integers(0, 2**32, size=600, dtype=np.uint32)
+    slots = list(range(600 // 16))
+    e.prefill(t, [1, 2], 0, slots)
+    e.prefill(t, [1, 2], 512, slots)
+torch.cuda.synchronize()
+print("sanitize workload done")
