@@ -13,8 +13,8 @@ What it restates (numpy, float64 arithmetic):
     and rests on the definitions stated here and in DESIGN.md, cross-checked against transformers' Llama.
   * the engine's counter-hash weight init, bit for bit (csrc/kernels.cu: unit_uniform / init kernels).
 
-bf16-faithful: values are rounded to bf16 at the same storage points as the kernels (normed activations,
-roped q/k, v, attention output, SiLU.mul output, final hidden); accumulation is float64.
+bf16-faithful: values are rounded to bf16 at the same storage points as the kernels (the folded-RMSNorm GEMM
+input bf16(x . gamma), roped q/k, v, attention output, SiLU.mul output, final hidden); accumulation is float64.
 """
 
 from __future__ import annotations
@@ -240,6 +240,13 @@ def _exact(x):
     return np.asarray(x, dtype=np.float64)
 
 
+def folded_norm(x: np.ndarray, gamma: np.ndarray, eps: float, rnd) -> tuple[np.ndarray, np.ndarray]:
+    """The engine's RMSNorm, folded across the next GEMM: returns (rnd(x . gamma), 1/rms per row); the GEMM
+    output row is multiplied by 1/rms (csrc/gemm.cu row_inv_rms). Exact algebra equals rnd-free rmsnorm."""
+    inv = 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps)
+    return rnd(x * gamma), inv
+
+
 def apply_rope(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
     """Rotate-half RoPE on (n, H, d): pairs (i, i + d/2)."""
     half = x.shape[-1] // 2
@@ -267,10 +274,10 @@ def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_
         cos, sin = np.cos(ang), np.sin(ang)
     x = w["embed"][toks.astype(np.int64)].astype(np.float64)
     for lw in w["layers"]:
-        xn = rmsnorm(x, lw["attn_norm"], cfg.rms_eps, R)
-        q = xn @ lw["wq"].T.astype(np.float64)
-        k = xn @ lw["wk"].T.astype(np.float64)
-        v = xn @ lw["wv"].T.astype(np.float64)
+        xg, inv = folded_norm(x, lw["attn_norm"], cfg.rms_eps, R)
+        q = inv * (xg @ lw["wq"].T.astype(np.float64))
+        k = inv * (xg @ lw["wk"].T.astype(np.float64))
+        v = inv * (xg @ lw["wv"].T.astype(np.float64))
         if "bqkv" in lw:  # Qwen2: bias added to the projections before RoPE
             b = lw["bqkv"].astype(np.float64)
             q, k, v = q + b[: hq * hd], k + b[hq * hd:(hq + hkv) * hd], v + b[(hq + hkv) * hd:]
@@ -280,9 +287,11 @@ def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_
         v = R(v)
         ctx = R(causal_attention(q, k, v)).reshape(n, hq * hd)
         x = x + ctx @ lw["wo"].T.astype(np.float64)
-        xn2 = rmsnorm(x, lw["mlp_norm"], cfg.rms_eps, R)
-        x = x + gated_mlp(xn2, lw["w_gate"].T.astype(np.float64), lw["w_up"].T.astype(np.float64),
-                          lw["w_down"].T.astype(np.float64), round_act=round_bf16)
+        xg2, inv2 = folded_norm(x, lw["mlp_norm"], cfg.rms_eps, R)
+        g = inv2 * (xg2 @ lw["w_gate"].T.astype(np.float64))
+        u = inv2 * (xg2 @ lw["w_up"].T.astype(np.float64))
+        act = R(silu(g) * u)
+        x = x + act @ lw["w_down"].T.astype(np.float64)
     h_last = rmsnorm(x[-1:], w["final_norm"], cfg.rms_eps, R)[0]
     alw = np.asarray(allowed, dtype=np.int64)
     logits = w["lm_head"][alw].astype(np.float64) @ h_last

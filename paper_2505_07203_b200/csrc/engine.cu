@@ -49,7 +49,10 @@ struct po_engine {
   std::vector<Layer> layers;
   // arena
   float* resid = nullptr;
-  __nv_bfloat16* xn = nullptr;  // also the attention output (ctx)
+  __nv_bfloat16* xn = nullptr;  // attention output (ctx)
+  __nv_bfloat16* xg = nullptr;  // bf16(resid . gamma): the folded-RMSNorm GEMM input (see GemmArgs)
+  float* ss_attn = nullptr;     // per-row, per-128-column sums of resid^2 feeding the next attention norm
+  float* ss_mlp = nullptr;      // ... feeding the next MLP norm
   __nv_bfloat16* qkv = nullptr;
   __nv_bfloat16* act = nullptr;
   float2* rope = nullptr;
@@ -57,7 +60,7 @@ struct po_engine {
   size_t gemm_ws_bytes = 0;
   void* attn_ws = nullptr;  // split-KV partials for short-query (prefix-hit) requests
   size_t attn_ws_bytes = 0;
-  CUtensorMap map_xn, map_ctx, map_act;
+  CUtensorMap map_xn, map_ctx, map_act, map_xg;
   // per-request device staging
   uint32_t* d_tokens = nullptr;
   int* d_slots = nullptr;
@@ -247,6 +250,9 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
   if (dalloc(e, &e->resid, (size_t)T * h * 4, &e->arena_bytes) ||
       dalloc(e, &e->xn, (size_t)T * xcols * 2, &e->arena_bytes) ||
       dalloc(e, &e->qkv, (size_t)T * qkvc * 2, &e->arena_bytes) ||
+      dalloc(e, &e->xg, (size_t)T * h * 2, &e->arena_bytes) ||
+      dalloc(e, &e->ss_attn, (size_t)T * (h / 128) * 4, &e->arena_bytes) ||
+      dalloc(e, &e->ss_mlp, (size_t)T * (h / 128) * 4, &e->arena_bytes) ||
       dalloc(e, &e->act, (size_t)chunk_rows * I * 2, &e->arena_bytes) ||
       dalloc(e, &e->rope, (size_t)T * (c.head_dim / 2) * sizeof(float2), &e->arena_bytes))
     return fail(PO_ERR_CUDA, "arena allocation failed");
@@ -300,6 +306,7 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     cudaStreamSynchronize(s);
   }
   if (po::make_tmap_a(&e->map_xn, e->xn, h, T, h) || po::make_tmap_a(&e->map_ctx, e->xn, ctxc, T, ctxc) ||
+      po::make_tmap_a(&e->map_xg, e->xg, h, T, h) ||
       po::make_tmap_a(&e->map_act, e->act, I, chunk_rows, I))
     return fail(PO_ERR_CUDA, "activation tensor-map encode failed");
 
@@ -471,17 +478,24 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
   if (cached_blocks) cudaMemcpyAsync(e->d_slots, e->h_slots, (size_t)cached_blocks * 4, cudaMemcpyHostToDevice, s);
   if (n_admit) cudaMemcpyAsync(e->d_admit, e->h_admit, (size_t)n_admit * 8, cudaMemcpyHostToDevice, s);
 
+  // RMSNorm is folded across the GEMMs (GemmArgs): producers (embedding, residual epilogues) write
+  // xg = bf16(resid . gamma_next) and per-segment sums of squares; consumers scale rows by 1/rms.
+  const int nseg = h / 128;
   mark(KC_EMBED, true);
-  po::launch_embed(d_tok_miss, n_miss, e->embed, c.vocab, h, e->resid, s);
+  po::launch_embed_norm(d_tok_miss, n_miss, e->embed, c.vocab, h, e->layers[0].attn_norm, e->resid, e->xg,
+                        e->ss_attn, s);
   mark(KC_EMBED, false);
   ++launches;
+  auto norm_in = [&](po::GemmArgs& g, const float* ss) {
+    g.ss_in = ss; g.ss_nseg = nseg; g.norm_eps = c.rms_eps; g.norm_dim = h;
+  };
+  auto norm_out = [&](po::GemmArgs& g, __nv_bfloat16* xg, const float* gamma, float* ss) {
+    g.xg_out = xg; g.ldxg = h; g.g_next = gamma; g.ss_out = ss; g.ss_nseg = nseg;
+  };
   int rc = 0;
   for (int l = 0; l < L && !rc; ++l) {
     auto& ly = e->layers[l];
-    mark(KC_NORM, true);
-    po::launch_rmsnorm(e->resid, n_miss, h, ly.attn_norm, c.rms_eps, e->xn, s);
-    mark(KC_NORM, false);
-    ++launches;
+    const float* gamma_next_layer = l + 1 < L ? e->layers[l + 1].attn_norm : e->final_norm;
     if (n_c > 0) {
       mark(KC_GATHER, true);
       po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
@@ -494,8 +508,9 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
     g.split_ws = e->gemm_ws;
     g.bias = ly.bqkv;
+    norm_in(g, e->ss_attn);
     mark(KC_QKV, true);
-    rc |= gemm(e->map_xn, ly.map_qkv, ly.map2_qkv, po::EPI_QKV_ROPE, g, s);
+    rc |= gemm(e->map_xg, ly.map_qkv, ly.map2_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
     ++launches;
     if (n_admit) {
@@ -518,28 +533,28 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     po::GemmArgs go{};
     go.M = rows; go.N = h; go.K = ctxc;
     go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
+    norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     mark(KC_O, true);
     rc |= gemm(e->map_ctx, ly.map_o, ly.map2_o, po::EPI_RESID_F32, go, s);
     mark(KC_O, false);
     ++launches;
     for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
       const int cr = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
-      mark(KC_NORM, true);
-      po::launch_rmsnorm(e->resid + (size_t)lo * h, cr, h, ly.mlp_norm, c.rms_eps, e->xn + (size_t)lo * h, s);
-      mark(KC_NORM, false);
       po::GemmArgs gu{};
       gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
+      norm_in(gu, e->ss_mlp + (size_t)lo * nseg);
       mark(KC_GATE_UP, true);
-      rc |= gemm(e->map_xn, ly.map_gu, ly.map2_gu, po::EPI_SILU_MUL, gu, s);
+      rc |= gemm(e->map_xg, ly.map_gu, ly.map2_gu, po::EPI_SILU_MUL, gu, s);
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
+      norm_out(gd, e->xg + (size_t)lo * h, gamma_next_layer, e->ss_attn + (size_t)lo * nseg);
       mark(KC_DOWN, true);
       rc |= gemm(e->map_act, ly.map_down, ly.map2_down, po::EPI_RESID_F32, gd, s);
       mark(KC_DOWN, false);
-      launches += 3;
+      launches += 2;
     }
   }
   if (rc) return set_error(PO_ERR_CUDA, "po_prefill: kernel launch failed (%d): %s", rc,

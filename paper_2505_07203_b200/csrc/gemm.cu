@@ -38,8 +38,18 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& m_
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
+// 1/rms of output row `row` from the producer's per-segment sums of squares (fixed summation order)
+__device__ __forceinline__ float row_inv_rms(const GemmArgs& a, int row) {
+  const float* p = a.ss_in + (long long)row * a.ss_nseg;
+  float s = 0.f;
+  for (int i = 0; i < a.ss_nseg; ++i) s += p[i];
+  return rsqrtf(s / a.norm_dim + a.norm_eps);
+}
+
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int col0, const uint32_t (&r)[32]) {
+__device__ __forceinline__ float epilogue_chunk(const GemmArgs& a, int row, int col0, const uint32_t (&r)[32],
+                                                float sc = 1.0f) {
+  float sq = 0.f;
   if constexpr (EPI == EPI_BF16) {
     uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col0);
 #pragma unroll
@@ -59,17 +69,32 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int c
                            __uint_as_float(r[4 * q + 3]));
   } else if constexpr (EPI == EPI_RESID_F32) {
     float4* dst = reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col0);
+    float4 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = dst[q];  // all loads in flight first
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float4 v = dst[q];
-      v.x += __uint_as_float(r[4 * q + 0]);
-      v.y += __uint_as_float(r[4 * q + 1]);
-      v.z += __uint_as_float(r[4 * q + 2]);
-      v.w += __uint_as_float(r[4 * q + 3]);
-      dst[q] = v;
+      v[q].x += __uint_as_float(r[4 * q + 0]);
+      v[q].y += __uint_as_float(r[4 * q + 1]);
+      v[q].z += __uint_as_float(r[4 * q + 2]);
+      v[q].w += __uint_as_float(r[4 * q + 3]);
+      dst[q] = v[q];
+    }
+    if (a.xg_out) {
+      const float4* g4 = reinterpret_cast<const float4*>(a.g_next + col0);
+      uint4* xo = reinterpret_cast<uint4*>(a.xg_out + (long long)row * a.ldxg + col0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 ga = g4[2 * q], gb = g4[2 * q + 1];
+        const float4 va = v[2 * q], vb = v[2 * q + 1];
+        xo[q] = make_uint4(pack_bf16(va.x * ga.x, va.y * ga.y), pack_bf16(va.z * ga.z, va.w * ga.w),
+                           pack_bf16(vb.x * gb.x, vb.y * gb.y), pack_bf16(vb.z * gb.z, vb.w * gb.w));
+        sq += va.x * va.x + va.y * va.y + va.z * va.z + va.w * va.w + vb.x * vb.x + vb.y * vb.y + vb.z * vb.z +
+              vb.w * vb.w;
+      }
     }
   } else if constexpr (EPI == EPI_SILU_MUL) {
-    // 32 accumulator columns = 16 gate columns followed by the matching 16 up columns.
+    // 32 accumulator columns = 16 gate columns followed by the matching 16 up columns; sc = this row's 1/rms
     uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col0 / 2);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -77,13 +102,14 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int c
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int j = 8 * q + 2 * e;
-        const float x0 = silu_f(__uint_as_float(r[j])) * __uint_as_float(r[16 + j]);
-        const float x1 = silu_f(__uint_as_float(r[j + 1])) * __uint_as_float(r[16 + j + 1]);
+        const float x0 = silu_f(sc * __uint_as_float(r[j])) * (sc * __uint_as_float(r[16 + j]));
+        const float x1 = silu_f(sc * __uint_as_float(r[j + 1])) * (sc * __uint_as_float(r[16 + j + 1]));
         w[e] = pack_bf16(x0, x1);
       }
       dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+  return sq;
 }
 
 // Epilogue of one 128-row x 256-column accumulator (this thread: TMEM lane = output row `row`).
@@ -103,6 +129,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
     }
   } else if constexpr (EPI == EPI_QKV_ROPE) {
     // two 128-column heads per tile; rotate-half pairs (i, i+64)
+    const float sc = (args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       const int hcol = nb * BN + h * 128;
@@ -114,6 +141,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
         tmem_ld32(taddr + h * 128 + half * 32, x1);
         tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
         tmem_ld_wait();
+        if (args.ss_in) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            x1[i] = __float_as_uint(sc * __uint_as_float(x1[i]));
+            x2[i] = __float_as_uint(sc * __uint_as_float(x2[i]));
+          }
+        }
         if (args.bias) {
           const float* b1 = args.bias + hcol + half * 32;
 #pragma unroll
@@ -138,13 +172,27 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
         }
       }
     }
-  } else {
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    float sq[2] = {0.f, 0.f};
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
-      if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BN + c, r);
+      if (row < args.M) sq[c >> 7] += epilogue_chunk<EPI>(args, row, nb * BN + c, r);
+    }
+    if (args.ss_out && row < args.M) {
+      args.ss_out[(long long)row * args.ss_nseg + 2 * nb] = sq[0];
+      args.ss_out[(long long)row * args.ss_nseg + 2 * nb + 1] = sq[1];
+    }
+  } else {
+    const float sc = (EPI == EPI_SILU_MUL && args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BN + c, r, sc);
     }
   }
 }
@@ -424,6 +472,11 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       const float4 v = *reinterpret_cast<const float4*>(p + s * slice);
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
+    float sc = 1.0f;
+    if constexpr (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
+      if (a.ss_in) sc = row_inv_rms(a, row);
+      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+    }
     if constexpr (EPI == EPI_BF16) {
       *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
           make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
@@ -434,6 +487,16 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       float4 v = *d;
       v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
       *d = v;
+      if (a.xg_out) {
+        // N % 128 == 0: each warp covers one 128-column segment of one row (warps stay converged)
+        const float4 g = *reinterpret_cast<const float4*>(a.g_next + col);
+        *reinterpret_cast<uint2*>(a.xg_out + (long long)row * a.ldxg + col) =
+            make_uint2(pack_bf16(v.x * g.x, v.y * g.y), pack_bf16(v.z * g.z, v.w * g.w));
+        float sq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if ((threadIdx.x & 31) == 0) a.ss_out[(long long)row * a.ss_nseg + col / 128] = sq;
+      }
     } else if constexpr (EPI == EPI_SILU_MUL) {
       // 16-column groups: [gate 16 | up 16]; this thread's 4 columns are gate or up of output cols
       const int grp = col / 32, w = col % 32;
@@ -443,6 +506,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
           const float4 v = *reinterpret_cast<const float4*>(p + 16 + s * slice);
           up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
         }
+        up.x *= sc; up.y *= sc; up.z *= sc; up.w *= sc;
         const int oc = grp * 16 + w;
         *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
             make_uint2(pack_bf16(silu_f(acc.x) * up.x, silu_f(acc.y) * up.y),
@@ -459,6 +523,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
           const float4 v = *reinterpret_cast<const float4*>(p + 64 + s * slice);
           x2.x += v.x; x2.y += v.y; x2.z += v.z; x2.w += v.w;
         }
+        x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
         if (a.bias) {
           x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
         }

@@ -23,6 +23,19 @@ struct GemmArgs {
   int pos_offset;       // absolute position of row 0
   int rope_cols;        // columns [0, rope_cols) are rotated (q and k heads)
   const float* bias;    // EPI_QKV_ROPE: optional per-column bias added before RoPE (Qwen2 q/k/v bias)
+  // Fused RMSNorm (the norm is folded across the GEMM: (x/rms . g) W^T = (1/rms) ((x . g) W^T)):
+  //  consumer side (EPI_QKV_ROPE, EPI_SILU_MUL): A holds bf16(x . g); the epilogue scales each output row by
+  //    rsqrt(sum_seg ss_in[row][seg] / norm_dim + eps) before bias / RoPE / SiLU.
+  //  producer side (EPI_RESID_F32): after resid += acc, also write xg_out[row][col] = bf16(resid . g_next[col])
+  //    and ss_out[row][seg] = sum of resid^2 over 128-column segment seg (two per 256-column tile).
+  const float* ss_in;
+  int ss_nseg;          // 128-column segments per row (= hidden / 128)
+  float norm_eps;
+  int norm_dim;
+  __nv_bfloat16* xg_out;
+  long long ldxg;
+  const float* g_next;
+  float* ss_out;
   // split-K (small-M GEMMs, e.g. prefix-hit requests): k_splits > 1 writes fp32 partials to `split_ws`
   // ([k_splits][M][N]) and a reduce kernel applies the epilogue after summing in a fixed order.
   int k_splits;

@@ -70,76 +70,36 @@ void launch_init_norm(float* dst, long long n, uint64_t seed, uint32_t tid, cuda
   init_norm_kernel<<<64, 256, 0, s>>>(dst, n, seed, tid);
 }
 
-// ------------------------------------------------------------------ embedding
-__global__ void embed_kernel(const uint32_t* __restrict__ tokens, int n, const __nv_bfloat16* __restrict__ embed,
-                             int vocab, int hidden, float* __restrict__ resid) {
-  const int vec = hidden / 8;  // uint4 = 8 bf16
-  const long long total = (long long)n * vec;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = static_cast<int>(i / vec);
-    const int q = static_cast<int>(i - (long long)r * vec);
-    const uint32_t tok = tokens[r] % static_cast<uint32_t>(vocab);
-    const uint4 v = reinterpret_cast<const uint4*>(embed + (long long)tok * hidden)[q];
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
-    float4* d = reinterpret_cast<float4*>(resid + (long long)r * hidden + q * 8);
+// ------------------------------------------------------------------ embedding (+ first folded-RMSNorm input)
+// one CTA (8 warps) per row; warp w handles 128-column segments w, w + 8, ... (32 lanes x 4 columns)
+__global__ void __launch_bounds__(256) embed_norm_kernel(const uint32_t* __restrict__ tokens,
+                                                         const __nv_bfloat16* __restrict__ embed, int vocab,
+                                                         int hidden, const float* __restrict__ gamma,
+                                                         float* __restrict__ resid, __nv_bfloat16* __restrict__ xg,
+                                                         float* __restrict__ ss) {
+  const long long r = blockIdx.x;
+  const uint32_t tok = tokens[r] % static_cast<uint32_t>(vocab);
+  const int nseg = hidden / 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int seg = warp; seg < nseg; seg += 8) {
+    const int col = seg * 128 + lane * 4;
+    const uint2 raw = *reinterpret_cast<const uint2*>(embed + (long long)tok * hidden + col);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
     const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
-    const float2 f2 = __bfloat1622float2(b[2]), f3 = __bfloat1622float2(b[3]);
-    d[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
-    d[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+    *reinterpret_cast<float4*>(resid + r * hidden + col) = make_float4(f0.x, f0.y, f1.x, f1.y);
+    const float4 g = *reinterpret_cast<const float4*>(gamma + col);
+    *reinterpret_cast<uint2*>(xg + r * hidden + col) =
+        make_uint2(pack_bf16(f0.x * g.x, f0.y * g.y), pack_bf16(f1.x * g.z, f1.y * g.w));
+    float sq = f0.x * f0.x + f0.y * f0.y + f1.x * f1.x + f1.y * f1.y;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) ss[r * nseg + seg] = sq;
   }
 }
-void launch_embed(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden, float* resid,
-                  cudaStream_t s) {
+void launch_embed_norm(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden,
+                       const float* gamma, float* resid, __nv_bfloat16* xg, float* ss, cudaStream_t s) {
   if (n <= 0) return;
-  embed_kernel<<<148 * 16, 256, 0, s>>>(tokens, n, embed, vocab, hidden, resid);
-}
-
-// ------------------------------------------------------------------ RMSNorm (one CTA per row)
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int hidden,
-                                                      const float* __restrict__ gamma, float eps,
-                                                      __nv_bfloat16* __restrict__ out) {
-  __shared__ float red[32];
-  const long long row = blockIdx.x;
-  const float4* xr = reinterpret_cast<const float4*>(x + row * hidden);
-  const int nv = hidden / 4;
-  float4 cache[8];
-  float ss = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int q = threadIdx.x + k * 256;
-    if (q < nv) {
-      cache[k] = xr[q];
-      ss += cache[k].x * cache[k].x + cache[k].y * cache[k].y + cache[k].z * cache[k].z + cache[k].w * cache[k].w;
-    }
-  }
-  for (int q = threadIdx.x + 8 * 256; q < nv; q += 256) {
-    const float4 v = xr[q];
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-  }
-  ss = block_sum(ss, red);
-  const float inv = rsqrtf(ss / hidden + eps);
-  const float4* g4 = reinterpret_cast<const float4*>(gamma);
-  uint2* o2 = reinterpret_cast<uint2*>(out + row * hidden);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int q = threadIdx.x + k * 256;
-    if (q < nv) {
-      const float4 g = g4[q];
-      const float4 v = cache[k];
-      o2[q] = make_uint2(pack_bf16(v.x * inv * g.x, v.y * inv * g.y), pack_bf16(v.z * inv * g.z, v.w * inv * g.w));
-    }
-  }
-  for (int q = threadIdx.x + 8 * 256; q < nv; q += 256) {
-    const float4 g = g4[q];
-    const float4 v = xr[q];
-    o2[q] = make_uint2(pack_bf16(v.x * inv * g.x, v.y * inv * g.y), pack_bf16(v.z * inv * g.z, v.w * inv * g.w));
-  }
-}
-void launch_rmsnorm(const float* x, int rows, int hidden, const float* gamma, float eps, __nv_bfloat16* out,
-                    cudaStream_t s) {
-  if (rows <= 0) return;
-  rmsnorm_kernel<<<rows, 256, 0, s>>>(x, hidden, gamma, eps, out);
+  embed_norm_kernel<<<n, 256, 0, s>>>(tokens, embed, vocab, hidden, gamma, resid, xg, ss);
 }
 
 // ------------------------------------------------------------------ prefix pool <-> qkv

@@ -25,12 +25,10 @@ void launch_init_norm(float* dst, long long n, uint64_t seed, uint32_t tid, cuda
 // dst (fp32) = bf16(0.1 * u): random-init q/k/v bias
 void launch_init_bias(float* dst, long long n, uint64_t seed, uint32_t tid, cudaStream_t s);
 
-// resid[r, :] = float(embed[tokens[r] % vocab, :])
-void launch_embed(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden, float* resid,
-                  cudaStream_t s);
-// out[r, :] = bf16(x[r, :] * rsqrt(mean(x^2) + eps) * gamma)
-void launch_rmsnorm(const float* x, int rows, int hidden, const float* gamma, float eps, __nv_bfloat16* out,
-                    cudaStream_t s);
+// resid[r, :] = float(embed[tokens[r] % vocab, :]); xg[r, :] = bf16(resid . gamma); ss[r][seg] = sum of resid^2 over
+// 128-column segment seg (the first layer's folded RMSNorm input, see GemmArgs)
+void launch_embed_norm(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden,
+                       const float* gamma, float* resid, __nv_bfloat16* xg, float* ss, cudaStream_t s);
 // Prefix pool <-> layer qkv buffer. Pool layout: [slot][layer][block_tokens][kv_dim] bf16.
 void launch_kv_gather(const __nv_bfloat16* pool, const int* slots, int n_rows, int layer, int num_layers,
                       int block_tokens, int kv_dim, __nv_bfloat16* qkv, long long ld, int col0, cudaStream_t s);

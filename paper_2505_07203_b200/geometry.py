@@ -35,7 +35,8 @@ def intermediate_bytes_per_token(m: ModelConfig) -> int:
 def arena_bytes(m: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK) -> int:
     """Activation arena po_init allocates for `max_tokens` (hybrid prefill, one layer of K/V).
 
-    Mirrors csrc/engine.cu: resid fp32 [T,h] + xn/ctx bf16 [T,max(h,Hq*d)] + qkv bf16 [T,(Hq+2Hkv)*d]
+    Mirrors csrc/engine.cu: resid fp32 [T,h] + ctx bf16 [T,max(h,Hq*d)] + qkv bf16 [T,(Hq+2Hkv)*d]
+    + xg bf16 [T,h] + sum-of-squares fp32 2 x [T, h/128]
     + MLP chunk bf16 [min(chunk,T), I] + RoPE (cos,sin) fp32 [T, d/2] + per-request staging; the split-KV /
     split-K workspaces (short queries only) are excluded and bounded separately.
     """
@@ -45,6 +46,7 @@ def arena_bytes(m: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK) -> 
     qkvc = (m.n_heads + 2 * m.n_kv_heads) * hd
     rows = min(chunk, T)
     b = 4 * T * h + 2 * T * max(h, ctx) + 2 * T * qkvc + 2 * rows * m.intermediate + 8 * T * (hd // 2)
+    b += 2 * T * h + 2 * 4 * T * (h // 128)  # folded-RMSNorm input xg (bf16) + two sum-of-squares buffers
     max_blocks = T // 16 + 1
     b += 4 * T + 4 * max_blocks + 8 * max_blocks + 3 * 4 * m.vocab + 16
     return b
