@@ -271,6 +271,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();     // qkv of this layer (QKV GEMM, pool gather) complete
+  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {
@@ -439,6 +441,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml, int n_q,
                                     int hq, int splits, int tiles_per_split, int q_offset, int n_total, int span,
                                     __nv_bfloat16* __restrict__ out, long long ldo) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = (long long)n_q * hq * (HD / 4);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -511,7 +515,8 @@ void attention_split_plan(int n_total, int q_offset, int hq, int hkv, int* split
   const int max_tiles = (n_total - 1) / BKV + 1;
   int s = 1;
   if (base < 148 && max_tiles >= 8) {
-    s = (2 * 148 + base - 1) / base;
+    // equal-work CTAs, one per SM: fill exactly one wave (a second partial wave costs a whole extra wave)
+    s = 148 / base;
     s = min(s, max_tiles / 4);
     s = min(s, 32);
     s = max(s, 1);
@@ -568,12 +573,13 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
                                           (size_t)a.splits * a.n_q * hq * HD * sizeof(float));
   }
   const int grid = lay.ctas * a.splits;
-  attn_fwd_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(map, map_q, a);
+  launch_pdl(attn_fwd_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, stream, map, map_q, a);
   if (a.splits > 1) {
     const long long total = (long long)a.n_q * hq * (HD / 4);
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-    attn_combine_kernel<<<blocks, 256, 0, stream>>>(a.part_o, a.part_ml, a.n_q, hq, a.splits, a.tiles_per_split,
-                                                    q_offset, n_total, lay.span, a.out, ldo);
+    launch_pdl(attn_combine_kernel, dim3(blocks), dim3(256), 0, stream, (const float*)a.part_o,
+               (const float2*)a.part_ml, a.n_q, hq, a.splits, a.tiles_per_split, q_offset, n_total, lay.span, a.out,
+               ldo);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }

@@ -45,6 +45,7 @@ struct po_engine {
     float* bqkv = nullptr;  // q/k/v bias (qkv_bias models), fp32 holding bf16 values
     CUtensorMap map_qkv, map_o, map_gu, map_down;      // 256-row boxes (1-CTA kernel)
     CUtensorMap map2_qkv, map2_o, map2_gu, map2_down;  // 128-row boxes (2-CTA pair kernel)
+    CUtensorMap map3_qkv, map3_o, map3_gu, map3_down;  // 64-row boxes (narrow pair tiles, small M)
   };
   std::vector<Layer> layers;
   // arena
@@ -240,7 +241,9 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     if (po::make_tmap_b(&ly.map_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b(&ly.map_o, ly.wo, ctxc, h, ctxc) ||
         po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I) ||
         po::make_tmap_a(&ly.map2_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_a(&ly.map2_o, ly.wo, ctxc, h, ctxc) ||
-        po::make_tmap_a(&ly.map2_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_a(&ly.map2_down, ly.wdown, I, h, I))
+        po::make_tmap_a(&ly.map2_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_a(&ly.map2_down, ly.wdown, I, h, I) ||
+        po::make_tmap_b64(&ly.map3_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b64(&ly.map3_o, ly.wo, ctxc, h, ctxc) ||
+        po::make_tmap_b64(&ly.map3_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b64(&ly.map3_down, ly.wdown, I, h, I))
       return fail(PO_ERR_CUDA, "weight tensor-map encode failed");
   }
 
@@ -439,9 +442,9 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
 }
 
 // 2-CTA pair GEMM for M > 128 (256-row pair tiles), 1-CTA 128-row tiles below
-int gemm(const CUtensorMap& a, const CUtensorMap& b1, const CUtensorMap& b2, int epi, const po::GemmArgs& g,
-         cudaStream_t s) {
-  return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(a, b2, epi, g, s) : po::gemm_launch(a, b1, epi, g, s);
+int gemm(const CUtensorMap& a, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& b3, int epi,
+         const po::GemmArgs& g, cudaStream_t s) {
+  return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(a, b2, epi, g, s, &b3) : po::gemm_launch(a, b1, epi, g, s);
 }
 
 enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
@@ -510,7 +513,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.bias = ly.bqkv;
     norm_in(g, e->ss_attn);
     mark(KC_QKV, true);
-    rc |= gemm(e->map_xg, ly.map_qkv, ly.map2_qkv, po::EPI_QKV_ROPE, g, s);
+    rc |= gemm(e->map_xg, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
     ++launches;
     if (n_admit) {
@@ -535,7 +538,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     mark(KC_O, true);
-    rc |= gemm(e->map_ctx, ly.map_o, ly.map2_o, po::EPI_RESID_F32, go, s);
+    rc |= gemm(e->map_ctx, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go, s);
     mark(KC_O, false);
     ++launches;
     for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
@@ -545,14 +548,14 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
       norm_in(gu, e->ss_mlp + (size_t)lo * nseg);
       mark(KC_GATE_UP, true);
-      rc |= gemm(e->map_xg, ly.map_gu, ly.map2_gu, po::EPI_SILU_MUL, gu, s);
+      rc |= gemm(e->map_xg, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu, s);
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
       norm_out(gd, e->xg + (size_t)lo * h, gamma_next_layer, e->ss_attn + (size_t)lo * nseg);
       mark(KC_DOWN, true);
-      rc |= gemm(e->map_act, ly.map_down, ly.map2_down, po::EPI_RESID_F32, gd, s);
+      rc |= gemm(e->map_act, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd, s);
       mark(KC_DOWN, false);
       launches += 2;
     }

@@ -113,7 +113,7 @@ __device__ __forceinline__ float epilogue_chunk(const GemmArgs& a, int row, int 
 }
 
 // Epilogue of one 128-row x 256-column accumulator (this thread: TMEM lane = output row `row`).
-template <int EPI>
+template <int EPI, int BNT = BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t taddr, int row, int nb, int ksp, int t) {
   if (ksp > 1) {
     // split-K partial: raw fp32 tile into the workspace slice of this split
@@ -121,18 +121,18 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
     pa.out = args.split_ws + (size_t)(t % ksp) * args.M * args.N;
     pa.ldo = args.N;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 0; c < BNT; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
-      if (row < args.M) epilogue_chunk<EPI_F32>(pa, row, nb * BN + c, r);
+      if (row < args.M) epilogue_chunk<EPI_F32>(pa, row, nb * BNT + c, r);
     }
   } else if constexpr (EPI == EPI_QKV_ROPE) {
     // two 128-column heads per tile; rotate-half pairs (i, i+64)
     const float sc = (args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int hcol = nb * BN + h * 128;
+    for (int h = 0; h < BNT / 128; ++h) {
+      const int hcol = nb * BNT + h * 128;
       const bool rot = hcol < args.rope_cols;
       const float2* cs = args.rope + (long long)(args.pos_offset + row) * 64;
 #pragma unroll 1
@@ -175,24 +175,24 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
   } else if constexpr (EPI == EPI_RESID_F32) {
     float sq[2] = {0.f, 0.f};
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 0; c < BNT; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
-      if (row < args.M) sq[c >> 7] += epilogue_chunk<EPI>(args, row, nb * BN + c, r);
+      if (row < args.M) sq[c >> 7] += epilogue_chunk<EPI>(args, row, nb * BNT + c, r);
     }
     if (args.ss_out && row < args.M) {
-      args.ss_out[(long long)row * args.ss_nseg + 2 * nb] = sq[0];
-      args.ss_out[(long long)row * args.ss_nseg + 2 * nb + 1] = sq[1];
+#pragma unroll
+      for (int k = 0; k < BNT / 128; ++k) args.ss_out[(long long)row * args.ss_nseg + nb * (BNT / 128) + k] = sq[k];
     }
   } else {
     const float sc = (EPI == EPI_SILU_MUL && args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 0; c < BNT; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
-      if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BN + c, r, sc);
+      if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BNT + c, r, sc);
     }
   }
 }
@@ -238,6 +238,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();     // the previous kernel's outputs (our A operand / residual) are complete from here on
+  pdl_trigger();  // let the next kernel of the forward start its prologue on SMs we free
 
   if (warp == 0) {
     if (lane == 0) {
@@ -324,21 +326,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // leader's full barrier; MMA commits multicast to both CTAs' empty / tmem-full barriers; each CTA drains its
 // own 128 accumulator rows and reports to the leader's tmem-empty barrier.
 namespace {
-constexpr int STAGES2 = 6;
-constexpr int HALF_BYTES = 128 * BK * 2;             // 16 KB: 128 rows x 64 bf16
-constexpr int STAGE2_BYTES = 2 * HALF_BYTES;         // A half + B half per CTA
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+constexpr int HALF_BYTES = 128 * BK * 2;             // 16 KB: 128 rows x 64 bf16 (A half per CTA)
+template <int BNT>
+struct Pair {
+  static constexpr int B_BYTES = (BNT / 2) * BK * 2;  // B half per CTA
+  static constexpr int STAGE = HALF_BYTES + B_BYTES;
+  static constexpr int STAGES = 192 * 1024 / STAGE;  // 6 (BNT 256) or 8 (BNT 128)
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
 }  // namespace
 
-template <int EPI>
+template <int EPI, int BNT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const GemmArgs args) {
+  constexpr int STAGES2 = Pair<BNT>::STAGES;
+  constexpr int B_HALF = Pair<BNT>::B_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES2 * HALF_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * Pair<BNT>::STAGE);
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -350,7 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
   const int num_m = (args.M + 2 * BM - 1) / (2 * BM);
-  const int num_n = args.N / BN;
+  const int num_n = args.N / BNT;
   const int ksp = args.k_splits > 1 ? args.k_splits : 1;
   const int num_tiles = num_m * num_n * ksp;
   const int nk_total = args.K / BK;
@@ -369,12 +377,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 2 * BNT);
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // peer barriers initialised before any remote arrive / TMA completion
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -389,10 +399,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int k = 0; k < nk; ++k) {
           const int kb = kb0 + k;
           mbar_wait(&empty_bar[s], ph ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * STAGE2_BYTES);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * Pair<BNT>::STAGE);
           const uint32_t fb = full0 + s * 8;
           tma_load_2d_pair(sA + s * HALF_BYTES, &map_a, fb, kb * BK, args.a_row0 + mb * 2 * BM + rank * BM);
-          tma_load_2d_pair(sB + s * HALF_BYTES, &map_b, fb, kb * BK, nb * BN + rank * (BN / 2));
+          tma_load_2d_pair(sB + s * B_HALF, &map_b, fb, kb * BK, nb * BNT + rank * (BNT / 2));
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
       }
@@ -400,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN);
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BNT);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -409,14 +419,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t acc_ph = (it >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BNT;
         const int kb0 = (t % ksp) * kbps;
         const int nk = min(nk_total, kb0 + kbps) - kb0;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
           const uint64_t adesc = sdesc_kmajor_sw128(smem_u32(sA + s * HALF_BYTES));
-          const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sB + s * HALF_BYTES));
+          const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sB + s * B_HALF));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
@@ -439,8 +449,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
       const int row = mb * 2 * BM + rank * BM + wq * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      epilogue_tile<EPI>(args, taddr, row, nb, ksp, t);
+      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BNT;
+      epilogue_tile<EPI, BNT>(args, taddr, row, nb, ksp, t);
       tc_fence_before();
       named_bar_sync(1, 128);
       if (threadIdx.x == 128) mbar_arrive_cluster(tempty0 + acc * 8);
@@ -452,13 +462,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc_pair(tmem_base, 512);
+    tmem_dealloc_pair(tmem_base, 2 * BNT);
   }
 }
 
 // Split-K reduction: sum the partials in split order, then apply the epilogue (one thread per 4 columns).
 template <int EPI>
 __global__ void splitk_reduce_kernel(const GemmArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int ncol4 = a.N / 4;
   const long long total = (long long)a.M * ncol4;
   const size_t slice = (size_t)a.M * a.N;
@@ -589,6 +601,9 @@ int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, 
 int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K) {
   return make_tmap_2d_bf16(map, B, K, N, ldb * 2, BK, BN);
 }
+int make_tmap_b64(CUtensorMap* map, const void* B, long long ldb, int N, int K) {
+  return make_tmap_2d_bf16(map, B, K, N, ldb * 2, BK, BN / 4);
+}
 
 int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K) {
   if (M <= 0 || N % BN != 0 || K % BK != 0) return -3;
@@ -598,6 +613,7 @@ int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long 
   if (make_tmap_2d_bf16(&plan->map_a, A, K, M, lda * 2, BK, BM)) return -2;
   if (make_tmap_2d_bf16(&plan->map_b, B, K, N, ldb * 2, BK, BN)) return -2;
   if (make_tmap_2d_bf16(&plan->map_b2, B, K, N, ldb * 2, BK, BM)) return -2;
+  if (make_tmap_2d_bf16(&plan->map_b3, B, K, N, ldb * 2, BK, BM / 2)) return -2;
   return 0;
 }
 
@@ -614,11 +630,13 @@ static void split_plan(int M, int N, int K, int* splits, int* kbps) {
   *splits = (nk + *kbps - 1) / *kbps;
 }
 
+bool gemm_pair_narrow(int M, int N);
+
 size_t gemm_split_ws_bytes(int M, int N, int K) {
   int s, kbps;
   split_plan(M, N, K, &s, &kbps);
-  // pair kernel (M > 128): splits bounded by SM pairs / pair tiles
-  const int tiles_mn = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  // pair kernel (M > 128): splits bounded by SM pairs / pair tiles (narrow 256 x 128 tiles for small M)
+  const int tiles_mn = ((M + 2 * BM - 1) / (2 * BM)) * (N / (gemm_pair_narrow(M, N) ? 128 : BN));
   const int nk = K / BK;
   int s2 = 1;
   if (tiles_mn * 2 <= num_sms() / 2 && nk >= 16) {
@@ -630,17 +648,17 @@ size_t gemm_split_ws_bytes(int M, int N, int K) {
   return smax > 1 ? (size_t)smax * M * N * sizeof(float) : 0;
 }
 
-template <int EPI>
-static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, const GemmArgs& in,
-                       cudaStream_t stream) {
+template <int EPI, int BNT>
+static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, const GemmArgs& in,
+                         cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+    cudaFuncSetAttribute(gemm2_kernel<EPI, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Pair<BNT>::SMEM);
     configured = true;
   }
   GemmArgs args = in;
   args.k_splits = 1;
-  const int tiles_mn = ((args.M + 2 * BM - 1) / (2 * BM)) * (args.N / BN);
+  const int tiles_mn = ((args.M + 2 * BM - 1) / (2 * BM)) * (args.N / BNT);
   if (args.split_ws) {
     // pair tiles: split K while fewer than SM-pairs/2 tiles exist (small-M prefix-hit GEMMs)
     const int nk = args.K / BK;
@@ -659,13 +677,24 @@ static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, cons
   }
   const int tiles = tiles_mn * args.k_splits;
   const int npairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  gemm2_kernel<EPI><<<2 * npairs, NUM_THREADS, SMEM2_BYTES, stream>>>(map_a, map_b2, args);
+  launch_pdl(gemm2_kernel<EPI, BNT>, dim3(2 * npairs), dim3(NUM_THREADS), Pair<BNT>::SMEM, stream, map_a, map_b2,
+             args);
   if (args.k_splits > 1) {
     const long long total = (long long)args.M * (args.N / 4);
     const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
-    splitk_reduce_kernel<EPI><<<blocks, 256, 0, stream>>>(args);
+    launch_pdl(splitk_reduce_kernel<EPI>, dim3(blocks), dim3(256), 0, stream, args);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+// 256 x 128 pair tiles when one row-tile of 256 x 256 tiles would leave most SM pairs idle (prefix hits)
+bool gemm_pair_narrow(int M, int N) { return M <= 2 * BM && N / BN < num_sms() / 2 && N % 128 == 0; }
+
+template <int EPI>
+static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, const CUtensorMap* map_b3,
+                       const GemmArgs& in, cudaStream_t stream) {
+  if (map_b3 && gemm_pair_narrow(in.M, in.N)) return launch_pair_t<EPI, 128>(map_a, *map_b3, in, stream);
+  return launch_pair_t<EPI, 256>(map_a, map_b2, in, stream);
 }
 
 template <int EPI>
@@ -687,25 +716,25 @@ static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const Gemm
   }
   const int tiles = ((args.M + BM - 1) / BM) * (args.N / BN) * args.k_splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_kernel<EPI><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(map_a, map_b, args);
+  launch_pdl(gemm_kernel<EPI>, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, stream, map_a, map_b, args);
   if (args.k_splits > 1) {
     const long long total = (long long)args.M * (args.N / 4);
     const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
-    splitk_reduce_kernel<EPI><<<blocks, 256, 0, stream>>>(args);
+    launch_pdl(splitk_reduce_kernel<EPI>, dim3(blocks), dim3(256), 0, stream, args);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
 int gemm_launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, int epi, const GemmArgs& args,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, const CUtensorMap* map_b3) {
   if (args.M <= 0) return 0;
   if (args.N % BN || args.K % BK) return -3;
   switch (epi) {
-    case EPI_BF16: return launch_pair<EPI_BF16>(map_a, map_b2, args, stream);
-    case EPI_RESID_F32: return launch_pair<EPI_RESID_F32>(map_a, map_b2, args, stream);
-    case EPI_SILU_MUL: return launch_pair<EPI_SILU_MUL>(map_a, map_b2, args, stream);
-    case EPI_QKV_ROPE: return launch_pair<EPI_QKV_ROPE>(map_a, map_b2, args, stream);
-    case EPI_F32: return launch_pair<EPI_F32>(map_a, map_b2, args, stream);
+    case EPI_BF16: return launch_pair<EPI_BF16>(map_a, map_b2, map_b3, args, stream);
+    case EPI_RESID_F32: return launch_pair<EPI_RESID_F32>(map_a, map_b2, map_b3, args, stream);
+    case EPI_SILU_MUL: return launch_pair<EPI_SILU_MUL>(map_a, map_b2, map_b3, args, stream);
+    case EPI_QKV_ROPE: return launch_pair<EPI_QKV_ROPE>(map_a, map_b2, map_b3, args, stream);
+    case EPI_F32: return launch_pair<EPI_F32>(map_a, map_b2, map_b3, args, stream);
     default: return -3;
   }
 }
@@ -738,7 +767,7 @@ int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t str
   args.M = plan.M;
   args.N = plan.N;
   args.K = plan.K;
-  if (gemm_use_pair(args.M)) return gemm_launch_pair(plan.map_a, plan.map_b2, epi, args, stream);
+  if (gemm_use_pair(args.M)) return gemm_launch_pair(plan.map_a, plan.map_b2, epi, args, stream, &plan.map_b3);
   return gemm_launch(plan.map_a, plan.map_b, epi, args, stream);
 }
 

@@ -46,7 +46,8 @@ struct GemmArgs {
 struct GemmPlan {
   CUtensorMap map_a;
   CUtensorMap map_b;   // 256-row boxes (1-CTA kernel)
-  CUtensorMap map_b2;  // 128-row boxes (2-CTA pair kernel)
+  CUtensorMap map_b2;  // 128-row boxes (2-CTA pair kernel, 256 x 256 tiles)
+  CUtensorMap map_b3;  // 64-row boxes (2-CTA pair kernel, 256 x 128 tiles for small M)
   int M, N, K;
 };
 
@@ -62,7 +63,8 @@ int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, con
 size_t gemm_split_ws_bytes(int M, int N, int K);
 // 2-CTA pair variant (M > 128): map_b2 must be built with 128-row boxes (make_tmap_a on the weight).
 int gemm_launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, int epi, const GemmArgs& args,
-                     cudaStream_t stream);
+                     cudaStream_t stream, const CUtensorMap* map_b3 = nullptr);
+int make_tmap_b64(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, int K);
 bool gemm_use_pair(int M);  // pair kernel for M > 128 unless PO_GEMM_1CTA=1
 int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K);

@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const uint32_t* __restr
                                                          int hidden, const float* __restrict__ gamma,
                                                          float* __restrict__ resid, __nv_bfloat16* __restrict__ xg,
                                                          float* __restrict__ ss) {
+  pdl_wait();
+  pdl_trigger();
   const long long r = blockIdx.x;
   const uint32_t tok = tokens[r] % static_cast<uint32_t>(vocab);
   const int nseg = hidden / 128;
@@ -99,13 +101,15 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const uint32_t* __restr
 void launch_embed_norm(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden,
                        const float* gamma, float* resid, __nv_bfloat16* xg, float* ss, cudaStream_t s) {
   if (n <= 0) return;
-  embed_norm_kernel<<<n, 256, 0, s>>>(tokens, embed, vocab, hidden, gamma, resid, xg, ss);
+  launch_pdl(embed_norm_kernel, dim3(n), dim3(256), 0, s, tokens, embed, vocab, hidden, gamma, resid, xg, ss);
 }
 
 // ------------------------------------------------------------------ prefix pool <-> qkv
 __global__ void kv_gather_kernel(const __nv_bfloat16* __restrict__ pool, const int* __restrict__ slots, int n_rows,
                                  int layer, int num_layers, int bt, int kv_dim, __nv_bfloat16* __restrict__ qkv,
                                  long long ld, int col0) {
+  pdl_wait();
+  pdl_trigger();
   const int vec = kv_dim / 8;
   const long long total = (long long)n_rows * vec;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -120,6 +124,8 @@ __global__ void kv_gather_kernel(const __nv_bfloat16* __restrict__ pool, const i
 __global__ void kv_scatter_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int col0,
                                   const int2* __restrict__ admit, int n_admit, int layer, int num_layers, int bt,
                                   int kv_dim, __nv_bfloat16* __restrict__ pool) {
+  pdl_wait();
+  pdl_trigger();
   const int vec = kv_dim / 8;
   const long long total = (long long)n_admit * bt * vec;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -136,14 +142,14 @@ __global__ void kv_scatter_kernel(const __nv_bfloat16* __restrict__ qkv, long lo
 void launch_kv_gather(const __nv_bfloat16* pool, const int* slots, int n_rows, int layer, int num_layers,
                       int block_tokens, int kv_dim, __nv_bfloat16* qkv, long long ld, int col0, cudaStream_t s) {
   if (n_rows <= 0) return;
-  kv_gather_kernel<<<148 * 8, 256, 0, s>>>(pool, slots, n_rows, layer, num_layers, block_tokens, kv_dim, qkv, ld,
-                                            col0);
+  launch_pdl(kv_gather_kernel, dim3(148 * 8), dim3(256), 0, s, pool, slots, n_rows, layer, num_layers, block_tokens,
+             kv_dim, qkv, ld, col0);
 }
 void launch_kv_scatter(const __nv_bfloat16* qkv, long long ld, int col0, const int2* admit, int n_admit, int layer,
                        int num_layers, int block_tokens, int kv_dim, __nv_bfloat16* pool, cudaStream_t s) {
   if (n_admit <= 0) return;
-  kv_scatter_kernel<<<148 * 8, 256, 0, s>>>(qkv, ld, col0, admit, n_admit, layer, num_layers, block_tokens, kv_dim,
-                                             pool);
+  launch_pdl(kv_scatter_kernel, dim3(148 * 8), dim3(256), 0, s, qkv, ld, col0, admit, n_admit, layer, num_layers,
+             block_tokens, kv_dim, pool);
 }
 
 // ------------------------------------------------------------------ allowed-row LM head
@@ -155,6 +161,8 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
                                                        int* __restrict__ argmax) {
   extern __shared__ float h[];  // [hidden] normalised last-row hidden state (bf16 values)
   __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
   __shared__ float bmax[32];
   __shared__ int bidx[32];
   float ss = 0.f;
@@ -219,8 +227,8 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
 }
 void launch_lm_head(const float* resid_row, int hidden, const float* gamma, float eps, const __nv_bfloat16* w,
                     const int* allowed, int n_allowed, float* logits, float* probs, int* argmax, cudaStream_t s) {
-  lm_head_kernel<<<1, 1024, hidden * sizeof(float), s>>>(resid_row, hidden, gamma, eps, w, allowed, n_allowed, logits,
-                                                          probs, argmax);
+  launch_pdl(lm_head_kernel, dim3(1), dim3(1024), hidden * sizeof(float), s, resid_row, hidden, gamma, eps, w, allowed,
+             n_allowed, logits, probs, argmax);
 }
 
 }  // namespace po

@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <utility>
 
 namespace po {
 
@@ -283,5 +284,31 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
                    smem_u32(bar)),
                "h"(mask)
                : "memory");
+}
+}  // namespace po
+
+namespace po {
+// ---------------------------------------------------------------- programmatic dependent launch (PDL)
+// Kernels of the forward are launched with programmatic stream serialization: each one does its local setup
+// (barriers, TMEM, descriptor prefetch), then pdl_wait() blocks until the previous kernel in the stream has
+// completed and its memory is visible, and pdl_trigger() lets the next kernel start launching (its CTAs
+// overlap this kernel's tail). Nothing before pdl_wait() may read or write global data of the forward.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 }  // namespace po
