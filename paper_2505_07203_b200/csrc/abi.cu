@@ -16,6 +16,20 @@ int set_error(int code, const char* fmt, ...) {
   g_last_error = buf;
   return code;
 }
+
+// The op entry points take their scratch from the device's default stream-ordered pool. Keep freed blocks in the
+// pool (no release to the driver at every synchronisation), so a per-call workspace costs no driver allocation.
+void keep_pool_memory() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done = true;
+}
 }  // namespace po
 
 extern "C" {
@@ -43,6 +57,7 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
   args.pos_offset = pos_offset;
   args.rope_cols = rope_cols;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  po::keep_pool_memory();
   const size_t ws = po::gemm_split_ws_bytes(M, N, K);
   if (ws && cudaMallocAsync(reinterpret_cast<void**>(&args.split_ws), ws, st) != cudaSuccess)
     return po::set_error(PO_ERR_CUDA, "po_op_gemm: split-K workspace allocation failed");

@@ -25,6 +25,8 @@ namespace po {
 int set_error(int code, const char* fmt, ...);
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
                       uint32_t box_inner, uint32_t box_outer);
+int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                      uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 
 namespace {
 constexpr int HD = 128;
@@ -60,6 +62,21 @@ struct AttnArgs {
   int R;              // MODE_PACKED: query rows per head in a slot (128 / GQA group)
   int G;              // GQA group size (query heads per kv head)
   int num_units;      // CTAs per split: query blocks (HEADS x head pairs), block pairs x heads, or chunk pairs x kv
+  // Pool-direct keys: rows [0, n_pool) of K/V are read straight from the prefix pool ([slot][layer][16][kv_dim],
+  // block b of the request in slot pool_slots[b]) instead of a gathered copy in qkv; rows >= n_pool from qkv.
+  int n_pool;         // 0 = every key row from qkv
+  const int* pool_slots;
+  int pool_layer, pool_layers;  // map_pool block index = slot * pool_layers + pool_layer
+  int pool_kcol, pool_vcol;     // column of this launch's K / V head 0 within a pool row
+};
+
+// Pool-direct key source of one attention launch (see AttnArgs): the prefix pool [num_blocks][num_layers][16][kv_dim]
+// bf16 and the request's per-block slots.
+struct AttnPool {
+  const void* base;
+  const int* slots;
+  int n_rows;  // cached key rows (multiple of 16) read from the pool
+  int num_blocks, num_layers, layer, kv_dim, block_tokens;
 };
 
 // Slot layouts. HEADS: two query heads of one GQA group over the same 128-row query block (K/V shared).
@@ -398,9 +415,10 @@ __device__ unsigned long long g_attn_trace[TRACE_EVENTS * TRACE_TILES];
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_q,
+                    const __grid_constant__ CUtensorMap map_pool, const __grid_constant__ CUtensorMap map16,
                     const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sQ = smem;                       // 2 tiles
   uint8_t* sK = smem + 2 * TILE_BYTES;      // 2 stages
   uint8_t* sV = smem + 4 * TILE_BYTES;      // 2 stages
@@ -476,8 +494,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp >= 8) {
   if (ATTN_ONEPASS) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
   if (warp == 8) {
+    const uint64_t keep = l2_policy_evict_last();
     if (lane == 0) {
-      const uint64_t keep = l2_policy_evict_last();
       mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
       if (a.mode != MODE_PACKED) {
 #pragma unroll
@@ -495,32 +513,55 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               tma_load_2d(sQ + i * TILE_BYTES + half * BOX_BYTES + k * a.R * 128, &map_q, q_full,
                           (g * a.G + k) * HD + half * 64, i ? qs1 : qs0);
       }
-      const int kcol = a.hq * HD + g * HD;
-      const int vcol = (a.hq + a.hkv) * HD + g * HD;
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        // K of tile j+2 streams in as soon as the S MMAs of tile j are done, well before its P.V
-        attn_wait_long(&k_empty[st], ph ^ 1);
-        TR(14, j);
-#ifdef ATTN_NOLOAD
-        if (j >= 2) {  // timing experiment only: reuse the resident K/V stages, no SMEM writes
-          mbar_arrive(&k_full[st]);
-          mbar_wait(&v_empty[st], ph ^ 1);
-          mbar_arrive(&v_full[st]);
-          continue;
+    }
+    const int kcol = a.hq * HD + g * HD;
+    const int vcol = (a.hq + a.hkv) * HD + g * HD;
+    // Pool-direct tiles: lanes 0-7 hold the pool slots of the tile's eight 16-key blocks, fetched one tile ahead
+    auto tile_slots = [&](int jj) -> int {
+      const int blk = (t0 + jj) * (BKV / 16) + (lane & 7);
+      return (jj < n_tiles && blk * 16 < a.n_pool) ? __ldg(a.pool_slots + blk) : 0;
+    };
+    int nxt = a.n_pool > 0 ? tile_slots(0) : 0;
+    // one 128-key K or V tile: a 128-row box from qkv, or per 16-key block a pool box (cached rows) or a 16-row box
+    // from qkv (the miss rows of the tile straddling n_pool); 16-row boxes land at 2 KB steps (swizzle-consistent)
+    auto load_kv = [&](uint8_t* dst, uint64_t* bar, int col, int pcol, int kr, int cur) {
+      if (kr >= a.n_pool) {
+        if (lane == 0) {
+          tma_load_2d_hint(dst, &map, bar, col, kr, keep);
+          tma_load_2d_hint(dst + BOX_BYTES, &map, bar, col + 64, kr, keep);
         }
-#endif
-        mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
-        const int kr = (t0 + j) * BKV;
-        tma_load_2d_hint(sK + st * TILE_BYTES, &map, &k_full[st], kcol, kr, keep);
-        tma_load_2d_hint(sK + st * TILE_BYTES + BOX_BYTES, &map, &k_full[st], kcol + 64, kr, keep);
-        attn_wait_long(&v_empty[st], ph ^ 1);
-        TR(20, j);
-        mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
-        tma_load_2d_hint(sV + st * TILE_BYTES, &map, &v_full[st], vcol, kr, keep);
-        tma_load_2d_hint(sV + st * TILE_BYTES + BOX_BYTES, &map, &v_full[st], vcol + 64, kr, keep);
+        return;
       }
+      // lane b < 8 issues block b's two boxes (the TMA issue work of a pool tile spreads over 8 lanes)
+      if (lane < BKV / 16) {
+        const int r = kr + 16 * lane;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint8_t* d = dst + half * BOX_BYTES + lane * 2048;
+          if (r < a.n_pool)
+            tma_load_3d_hint(d, &map_pool, bar, pcol + half * 64, 0, cur * a.pool_layers + a.pool_layer, keep);
+          else
+            tma_load_2d_hint(d, &map16, bar, col + half * 64, r, keep);
+        }
+      }
+    };
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      const int cur = nxt;
+      if (a.n_pool > 0) nxt = tile_slots(j + 1);
+      // K of tile j+2 streams in as soon as the S MMAs of tile j are done, well before its P.V
+      attn_wait_long(&k_empty[st], ph ^ 1);
+      TR(14, j);
+      const int kr = (t0 + j) * BKV;
+      if (lane == 0) mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
+      __syncwarp();  // expect_tx before any lane's copies complete on the barrier
+      load_kv(sK + st * TILE_BYTES, &k_full[st], kcol, a.pool_kcol + g * HD, kr, cur);
+      attn_wait_long(&v_empty[st], ph ^ 1);
+      TR(20, j);
+      if (lane == 0) mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
+      __syncwarp();
+      load_kv(sV + st * TILE_BYTES, &v_full[st], vcol, a.pool_vcol + g * HD, kr, cur);
     }
     __syncwarp();
   } else if (warp == 9) {
@@ -918,12 +959,23 @@ size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv) {
 }
 
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
-                  cudaStream_t stream, void* workspace, size_t workspace_bytes) {
+                  cudaStream_t stream, void* workspace, size_t workspace_bytes, const AttnPool* pool) {
   if (hq % hkv) return -3;
   const AttnLayout lay = attention_layout(n_total, q_offset, hq, hkv);
-  CUtensorMap map, map_q;
+  CUtensorMap map, map_q, map_pool, map16;
   if (make_tmap_2d_bf16(&map, qkv, ld, n_total, ld * 2, 64, 128)) return -2;
   if (make_tmap_2d_bf16(&map_q, qkv, ld, n_total, ld * 2, 64, lay.R)) return -2;
+  const bool use_pool = pool && pool->n_rows > 0;
+  if (use_pool) {
+    if (pool->block_tokens != 16 || pool->n_rows % 16 || pool->n_rows > n_total) return -3;
+    if (make_tmap_3d_bf16(&map_pool, pool->base, pool->kv_dim, 16, (uint64_t)pool->num_blocks * pool->num_layers,
+                          (uint64_t)pool->kv_dim * 2, (uint64_t)pool->kv_dim * 2 * 16, 64, 16, 1))
+      return -2;
+    if (make_tmap_2d_bf16(&map16, qkv, ld, n_total, ld * 2, 64, 16)) return -2;
+  } else {
+    map_pool = map;
+    map16 = map;
+  }
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -944,6 +996,14 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
   a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
+  if (use_pool) {
+    a.n_pool = pool->n_rows;
+    a.pool_slots = pool->slots;
+    a.pool_layer = pool->layer;
+    a.pool_layers = pool->num_layers;
+    a.pool_kcol = 0;
+    a.pool_vcol = hkv * HD;
+  }
   attention_split_plan(n_total, q_offset, hq, hkv, &a.splits, &a.tiles_per_split);
   const size_t need = attention_workspace_bytes(n_total, q_offset, hq, hkv);
   if (a.splits > 1 && (!workspace || workspace_bytes < need)) {
@@ -956,7 +1016,7 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
                                           (size_t)a.splits * a.n_q * hq * HD * sizeof(float));
   }
   const int grid = lay.ctas * a.splits;
-  launch_pdl(attn_fwd_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, stream, map, map_q, a);
+  launch_pdl(attn_fwd_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, stream, map, map_q, map_pool, map16, a);
   if (a.splits > 1) {
     const long long total = (long long)a.n_q * hq * (HD / 4);
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
@@ -991,7 +1051,7 @@ extern "C" int po_op_attention(const void* qkv, int64_t ld, int32_t n_total, int
   void* ws = nullptr;
   if (ws_bytes && cudaMallocAsync(&ws, ws_bytes, st) != cudaSuccess)
     return po::set_error(PO_ERR_CUDA, "po_op_attention: workspace allocation failed");
-  int rc = po::attention_run(qkv, ld, n_total, q_offset, n_heads, n_kv_heads, out, ldo, st, ws, ws_bytes);
+  int rc = po::attention_run(qkv, ld, n_total, q_offset, n_heads, n_kv_heads, out, ldo, st, ws, ws_bytes, nullptr);
   if (ws) cudaFreeAsync(ws, st);
   if (rc) return po::set_error(PO_ERR_CUDA, "po_op_attention: failed (%d): %s", rc,
                                cudaGetErrorString(cudaGetLastError()));

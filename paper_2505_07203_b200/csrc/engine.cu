@@ -19,13 +19,22 @@
 #include "kernels.cuh"
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
+#include <chrono>
 #include <algorithm>
 #include <vector>
 
 namespace po {
 int set_error(int code, const char* fmt, ...);
+struct AttnPool {
+  const void* base;
+  const int* slots;
+  int n_rows;
+  int num_blocks, num_layers, layer, kv_dim, block_tokens;
+};
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
-                  cudaStream_t stream, void* workspace, size_t workspace_bytes);
+                  cudaStream_t stream, void* workspace, size_t workspace_bytes, const AttnPool* pool);
 size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv);
 }  // namespace po
 
@@ -84,6 +93,7 @@ struct po_engine {
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
   float last_ms = 0.f;
+  float last_enqueue_ms = 0.f;  // host time to enqueue the forward (launch-bound when it approaches last_ms)
   int last_launches = 0;
   // per-kernel-class CUDA-event timing (bench roofline)
   bool profiling = false;
@@ -346,6 +356,7 @@ int po_engine_info(po_engine* e, int64_t* out, int32_t n) {
 int po_last_service_ms(po_engine* e, float* ms) {
   if (!e || !ms) return set_error(PO_ERR_ARG, "po_last_service_ms: null argument");
   *ms = e->last_ms;
+  if (getenv("PO_ENQUEUE_TIMING")) fprintf(stderr, "enqueue %.3f ms service %.3f ms\n", e->last_enqueue_ms, e->last_ms);
   return PO_OK;
 }
 
@@ -447,6 +458,16 @@ int gemm(const CUtensorMap& a, const CUtensorMap& b1, const CUtensorMap& b2, con
   return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(a, b2, epi, g, s, &b3) : po::gemm_launch(a, b1, epi, g, s);
 }
 
+// PO_POOL_DIRECT=0 gathers the cached K/V into the layer buffer before attention (A/B runs)
+bool pool_direct_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("PO_POOL_DIRECT");
+    on = (v && v[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
               KC_COUNT };
 
@@ -499,7 +520,9 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
   for (int l = 0; l < L && !rc; ++l) {
     auto& ly = e->layers[l];
     const float* gamma_next_layer = l + 1 < L ? e->layers[l + 1].attn_norm : e->final_norm;
-    if (n_c > 0) {
+    // cached prefix K/V: read by attention straight from the pool (pool-direct), or gathered into qkv first
+    const bool pool_direct = n_c > 0 && pool_direct_enabled() && bt == 16;
+    if (n_c > 0 && !pool_direct) {
       mark(KC_GATHER, true);
       po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
       mark(KC_GATHER, false);
@@ -529,8 +552,10 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     const int rows = n - q_first;                      // query rows of attention / O / MLP
     const int row0 = q_first - n_c;                    // their offset inside the miss rows
     mark(KC_ATTN, true);
+    // whole cached blocks come from the pool (a fully cached request's last block too: its K/V are in the pool)
+    po::AttnPool ap{e->pool, e->d_slots, pool_direct ? cached_blocks * bt : 0, (int)e->pool_blocks, L, l, kvd, bt};
     rc |= po::attention_run(e->qkv, qkvc, n, q_first, c.n_heads, c.n_kv_heads, e->xn, ctxc, s, e->attn_ws,
-                            e->attn_ws_bytes);
+                            e->attn_ws_bytes, pool_direct ? &ap : nullptr);
     mark(KC_ATTN, false);
     ++launches;
     po::GemmArgs go{};
@@ -592,8 +617,10 @@ int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached
   cudaEventRecord(e->ev0, s);
   cudaMemcpyAsync(e->d_tokens, e->h_tokens, (size_t)n_miss * 4, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(e->d_allowed, e->h_allowed, (size_t)n_allowed * 4, cudaMemcpyHostToDevice, s);
+  const auto h0 = std::chrono::steady_clock::now();
   int rc = forward(e, e->d_tokens, n, n_c, n_admit, e->d_allowed, n_allowed, e->d_logits, e->d_probs, e->d_argmax, s);
   if (rc) return rc;
+  e->last_enqueue_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
   cudaMemcpyAsync(e->h_logits, e->d_logits, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(e->h_probs, e->d_probs, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(e->h_argmax, e->d_argmax, 4, cudaMemcpyDeviceToHost, s);

@@ -54,6 +54,9 @@ struct GemmPlan {
 // Host helpers (gemm.cu)
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
                       uint32_t box_inner, uint32_t box_outer);
+// 3-D map (d0 innermost, 128B swizzle), e.g. the prefix pool [slot*layer][block_tokens][kv_dim].
+int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                      uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K);
 int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& args, cudaStream_t stream);
 // A/B maps built once (weights at init, activation buffers at init with their max rows).
@@ -69,5 +72,6 @@ int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, 
 bool gemm_use_pair(int M);  // pair kernel for M > 128 unless PO_GEMM_1CTA=1
 int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int num_sms();
+
 
 }  // namespace po

@@ -168,3 +168,18 @@ def test_arena_matches_geometry_model():
             norms_fp32_extra = (2 * model.num_layers + 1) * model.hidden * 2  # norms held as fp32 on device
             assert e.weight_bytes == model.weight_bytes + norms_fp32_extra
             assert e.block_bytes == model.kv_bytes_per_token[1] * 16
+
+
+@pytest.mark.parametrize("n_cached", [16, 656, 1008])
+def test_pool_direct_straddling_tiles_match_oracle(tiny_engine, n_cached):
+    """Cached K/V read by attention straight from the pool: a cached prefix that ends inside a 128-key tile mixes
+    pool blocks and freshly computed qkv rows in one tile (16-key boxes from each source)."""
+    bt = 16
+    base = tokens_for(21, 1200)
+    slots = list(range(200, 200 + len(base) // bt))
+    tiny_engine.prefill(base, YES_NO, n_cached=0, pool_block_ids=slots)
+    req = np.concatenate([base[:n_cached], tokens_for(22, 300)])
+    ids = slots[: n_cached // bt] + [-1] * (len(req) // bt - n_cached // bt)
+    warm = tiny_engine.prefill(req, YES_NO, n_cached=n_cached, pool_block_ids=ids)
+    assert warm.n_cached == n_cached
+    check_against_oracle(TINY, warm, req, YES_NO, 42)
