@@ -453,9 +453,30 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
 }
 
 // 2-CTA pair GEMM for M > 128 (256-row pair tiles), 1-CTA 128-row tiles below
-int gemm(const CUtensorMap& a, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& b3, int epi,
-         const po::GemmArgs& g, cudaStream_t s) {
-  return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(a, b2, epi, g, s, &b3) : po::gemm_launch(a, b1, epi, g, s);
+bool bounded_a_enabled();
+
+// x / ldx: the activation buffer behind `a`. A launch whose rows stop short of its A tile (short miss suffixes, the
+// last layer's final row) gets a map bounded at its last row, so the padding rows of the 128-row boxes are
+// zero-filled by TMA instead of being read from memory (for M = 1 that is 127 wasted rows per weight tile).
+int gemm(const CUtensorMap& a, const void* x, long long ldx, const CUtensorMap& b1, const CUtensorMap& b2,
+         const CUtensorMap& b3, int epi, const po::GemmArgs& g, cudaStream_t s) {
+  const CUtensorMap* am = &a;
+  CUtensorMap bounded;
+  if (g.M % 128 != 0 && bounded_a_enabled()) {
+    if (po::make_tmap_a(&bounded, x, ldx, (long long)g.a_row0 + g.M, g.K)) return -2;
+    am = &bounded;
+  }
+  return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(*am, b2, epi, g, s, &b3) : po::gemm_launch(*am, b1, epi, g, s);
+}
+
+// PO_BOUNDED_A=0 keeps the whole-buffer activation maps (A/B runs)
+bool bounded_a_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("PO_BOUNDED_A");
+    on = (v && v[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 // PO_POOL_DIRECT=0 gathers the cached K/V into the layer buffer before attention (A/B runs)
@@ -536,7 +557,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.bias = ly.bqkv;
     norm_in(g, e->ss_attn);
     mark(KC_QKV, true);
-    rc |= gemm(e->map_xg, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
+    rc |= gemm(e->map_xg, e->xg, h, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
     ++launches;
     if (n_admit) {
@@ -563,7 +584,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     mark(KC_O, true);
-    rc |= gemm(e->map_ctx, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go, s);
+    rc |= gemm(e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go, s);
     mark(KC_O, false);
     ++launches;
     for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
@@ -573,14 +594,14 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
       norm_in(gu, e->ss_mlp + (size_t)lo * nseg);
       mark(KC_GATE_UP, true);
-      rc |= gemm(e->map_xg, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu, s);
+      rc |= gemm(e->map_xg, e->xg, h, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu, s);
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
       norm_out(gd, e->xg + (size_t)lo * h, gamma_next_layer, e->ss_attn + (size_t)lo * nseg);
       mark(KC_DOWN, true);
-      rc |= gemm(e->map_act, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd, s);
+      rc |= gemm(e->map_act, e->act, I, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd, s);
       mark(KC_DOWN, false);
       launches += 2;
     }
