@@ -38,11 +38,19 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& m_
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
-// 1/rms of output row `row` from the producer's per-segment sums of squares (fixed summation order)
+// 1/rms of output row `row` from the producer's per-segment sums of squares (fixed summation order; the loads go
+// out 8 at a time so their latency is paid once per 8 segments, not once per segment)
 __device__ __forceinline__ float row_inv_rms(const GemmArgs& a, int row) {
   const float* p = a.ss_in + (long long)row * a.ss_nseg;
   float s = 0.f;
-  for (int i = 0; i < a.ss_nseg; ++i) s += p[i];
+  for (int i0 = 0; i0 < a.ss_nseg; i0 += 8) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = i0 + i < a.ss_nseg ? p[i0 + i] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i0 + i < a.ss_nseg) s += x[i];
+  }
   return rsqrtf(s / a.norm_dim + a.norm_eps);
 }
 
@@ -467,6 +475,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 }
 
 // Split-K reduction: sum the partials in split order, then apply the epilogue (one thread per 4 columns).
+// Sum of the k-split partials at p, p + slice, ... in split order; all loads issued before the adds.
+__device__ __forceinline__ float4 split_sum(const float* p, size_t slice, int splits) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = 0; s0 < splits; s0 += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      v[k] = s0 + k < splits ? __ldcg(reinterpret_cast<const float4*>(p + (s0 + k) * slice)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (s0 + k < splits) {
+        acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
+      }
+    }
+  }
+  return acc;
+}
+
 template <int EPI>
 __global__ void splitk_reduce_kernel(const GemmArgs a) {
   pdl_wait();
@@ -479,11 +505,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
     const int row = static_cast<int>(i / ncol4);
     const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
     const float* p = a.split_ws + (size_t)row * a.N + col;
-    float4 acc = *reinterpret_cast<const float4*>(p);
-    for (int s = 1; s < a.k_splits; ++s) {
-      const float4 v = *reinterpret_cast<const float4*>(p + s * slice);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
+    float4 acc = split_sum(p, slice, a.k_splits);
     float sc = 1.0f;
     if constexpr (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
       if (a.ss_in) sc = row_inv_rms(a, row);
@@ -513,11 +535,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       // 16-column groups: [gate 16 | up 16]; this thread's 4 columns are gate or up of output cols
       const int grp = col / 32, w = col % 32;
       if (w < 16) {
-        float4 up = *reinterpret_cast<const float4*>(p + 16);
-        for (int s = 1; s < a.k_splits; ++s) {
-          const float4 v = *reinterpret_cast<const float4*>(p + 16 + s * slice);
-          up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
-        }
+        float4 up = split_sum(p + 16, slice, a.k_splits);
         up.x *= sc; up.y *= sc; up.z *= sc; up.w *= sc;
         const int oc = grp * 16 + w;
         *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
@@ -530,11 +548,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
         acc.x += a.bias[col]; acc.y += a.bias[col + 1]; acc.z += a.bias[col + 2]; acc.w += a.bias[col + 3];
       }
       if (col < a.rope_cols && head_col < 64) {
-        float4 x2 = *reinterpret_cast<const float4*>(p + 64);
-        for (int s = 1; s < a.k_splits; ++s) {
-          const float4 v = *reinterpret_cast<const float4*>(p + 64 + s * slice);
-          x2.x += v.x; x2.y += v.y; x2.z += v.z; x2.w += v.w;
-        }
+        float4 x2 = split_sum(p + 64, slice, a.k_splits);
         x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
         if (a.bias) {
           x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
@@ -702,7 +716,16 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
 }
 
 // 256 x 128 pair tiles when one row-tile of 256 x 256 tiles would leave most SM pairs idle (prefix hits)
-bool gemm_pair_narrow(int M, int N) { return M <= 2 * BM && N / BN < num_sms() / 2 && N % 128 == 0; }
+bool gemm_pair_narrow(int M, int N) {
+  // 256 x 128 pair tiles without split-K, or (default) 256 x 256 tiles + split-K: the wide tiles halve the activation
+  // re-reads per weight byte and measured 2% faster per prefix hit. PO_PAIR_NARROW=1 selects the narrow tiles.
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("PO_PAIR_NARROW");
+    mode = (v && v[0] == '1') ? 1 : 0;
+  }
+  return mode && M <= 2 * BM && N / BN < num_sms() / 2 && N % 128 == 0;
+}
 
 template <int EPI>
 static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, const CUtensorMap* map_b3,
