@@ -20,6 +20,7 @@
 #include "sm100.cuh"
 #include "../../include/prefillonly.h"
 #include <cmath>
+#include <cstdlib>
 
 namespace po {
 int set_error(int code, const char* fmt, ...);
@@ -68,6 +69,7 @@ struct AttnArgs {
   const int* pool_slots;
   int pool_layer, pool_layers;  // map_pool block index = slot * pool_layers + pool_layer
   int pool_kcol, pool_vcol;     // column of this launch's K / V head 0 within a pool row
+  int kv_band;                  // MODE_HEADS CTA order: kv heads per band (0 = all heads interleaved)
 };
 
 // Pool-direct key source of one attention launch (see AttnArgs): the prefix pool [num_blocks][num_layers][16][kv_dim]
@@ -439,16 +441,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // heaviest (longest causal extent) units first. Slot i of this CTA: head hs_i (first head of the kv group
   // when packed), first query position qs_i; rows_slot query rows per head in the slot.
-  const int unit = a.num_units - 1 - blockIdx.x / (a.splits * (a.mode == MODE_HEADS ? a.hkv * a.pairs
-                                                                : a.mode == MODE_QBLOCKS ? a.hq : a.hkv));
+  int unit = a.num_units - 1 - blockIdx.x / (a.splits * (a.mode == MODE_HEADS ? a.hkv * a.pairs
+                                                          : a.mode == MODE_QBLOCKS ? a.hq : a.hkv));
   int split, g, hs0, hs1, qs0, qs1;
   int rows_slot = BQ;
   if (a.mode == MODE_HEADS) {
-    const int per_qb = a.hkv * a.pairs * a.splits;
-    int rem = blockIdx.x % per_qb;
+    // kv_band > 0 (long sequences): CTAs run in bands of kv_band kv heads (heaviest query block first within a
+    // band), so the CTAs resident at any time share the K/V of a few heads and that working set stays in L2
+    const int band = a.kv_band > 0 ? a.kv_band : a.hkv;
+    const int per_qb = band * a.pairs * a.splits;
+    const int band_ctas = a.num_units * per_qb;
+    const int b = a.kv_band > 0 ? blockIdx.x / band_ctas : 0;
+    const int r = a.kv_band > 0 ? blockIdx.x % band_ctas : blockIdx.x;
+    unit = a.num_units - 1 - r / per_qb;
+    int rem = r % per_qb;
     split = rem % a.splits;
     rem /= a.splits;
-    g = rem / a.pairs;
+    g = b * band + rem / a.pairs;
     hs0 = g * (2 * a.pairs) + 2 * (rem % a.pairs);
     hs1 = hs0 + 1;
     qs0 = qs1 = a.q_offset + unit * BQ;
@@ -996,6 +1005,21 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
   a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
+  {
+    // K + V bytes of all kv heads: when they overflow ~1/3 of L2, band the CTA order by kv head
+    static int force = -2;
+    if (force == -2) force = getenv("PO_ATTN_KVBAND") ? atoi(getenv("PO_ATTN_KVBAND")) : -1;
+    const double kv_all = (double)n_total * hkv * HD * 2 * 2;
+    int band = 0;
+    if (force >= 0) {
+      band = force;
+    } else if (kv_all > 40e6) {
+      band = hkv;
+      while (band > 1 && (double)n_total * band * HD * 2 * 2 > 40e6) band /= 2;
+      while (band > 1 && hkv % band) --band;
+    }
+    a.kv_band = (lay.mode == MODE_HEADS && band > 0 && hkv % band == 0) ? band : 0;
+  }
   if (use_pool) {
     a.n_pool = pool->n_rows;
     a.pool_slots = pool->slots;
