@@ -369,6 +369,9 @@ def main():
     if not args.no_qps:
         qps = qps_at_slo(eng, M, world, rank, args.slo, dist if world > 1 else None)
 
+    # ---------------- prefix-hit forward (the serving path after a cache hit): an HBM-bound weight stream
+    hit = prefix_hit_roofline(eng, M, n, peaks) if rank == 0 and not args.no_qps else None
+
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -393,12 +396,37 @@ def main():
             "dtype": "bf16", "data": "synthetic (counter-hash random-init weights, seeded uint32 token streams)",
             "config": workload_config(args, world), "e2e": e2e, "gpu_launches": launches_per_step * K,
             "roofline": roofline, "roofline_by_kernel": by_kernel, "step_roofline": step_roofline,
-            "cpu_baseline": cpu, "qps_at_slo": qps, "clocks": clocks,
+            "cpu_baseline": cpu, "qps_at_slo": qps, "prefix_hit": hit, "clocks": clocks,
             "answer": {"argmax": results[-1].token, "probs": results[-1].probs.tolist()},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def prefix_hit_roofline(eng, M, n, peaks):
+    """A warm prefix-hit request (all but the last 160 tokens cached, block-aligned) measured back to back: device
+    service time and its HBM roofline. One hit streams every layer weight once plus the cached K/V of all layers
+    (read by attention straight from the pool), so its floor is those bytes at the measured copy bandwidth."""
+    toks = np.random.default_rng([7, 1, 0]).integers(0, 2 ** 32, size=n, dtype=np.uint32)
+    nb = n // 16
+    slots = list(range(nb))
+    eng.prefill(toks, ALLOWED, 0, slots)  # admit the prefix
+    nc = (n - 160) // 16 * 16
+    for _ in range(5):  # back-to-back hits settle the clocks after the cold forward
+        eng.prefill(toks, ALLOWED, nc, slots)
+    ts = sorted(eng.prefill(toks, ALLOWED, nc, slots).service_s for _ in range(15))
+    med = ts[len(ts) // 2]
+    lin_weights = M.weight_bytes - 2 * (2 * M.vocab * M.hidden)  # embedding / LM head rows are gathered, not streamed
+    kv = M.kv_bytes_per_token[1] * n
+    bytes_ = lin_weights + kv
+    achieved = bytes_ / med / 1e9
+    return {"n": n, "n_cached": nc, "service_ms_median": med * 1e3, "service_ms_min": ts[0] * 1e3,
+            "bytes_per_request": bytes_, "achieved_gbs": achieved, "peak_gbs": peaks["hbm_gbs"],
+            "frac": achieved / peaks["hbm_gbs"], "bound": "hbm",
+            "note": "algorithmic bytes = layer weights streamed once + cached K/V of all layers read once; "
+                    "back-to-back hits (inside a mixed serving run the clocks are still recovering from cold "
+                    "forwards: see qps_at_slo.measured_service_s.prefix_hit_median)"}
 
 
 def qps_at_slo(eng, M, world, rank, slo, dist):
