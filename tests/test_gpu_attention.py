@@ -106,3 +106,35 @@ def test_attention_diagonal_boundary(n, off):
     assert ((out.float() - ref).abs().max() / ref.abs().max()).item() < 1e-2
     v = qkv[off:, 384:512].float()
     assert ((out[:, :128].float() - v).abs().max()).item() < 0.05
+
+
+def ref_attention_rows(qkv, n_total, rows, hq, hkv):
+    """fp32 reference for selected query rows only (long sequences: the full score matrix would not fit)."""
+    hd = 128
+    x = qkv.float()
+    k = x[:, hq * hd:(hq + hkv) * hd].view(n_total, hkv, hd).repeat_interleave(hq // hkv, dim=1)
+    v = x[:, (hq + hkv) * hd:(hq + 2 * hkv) * hd].view(n_total, hkv, hd).repeat_interleave(hq // hkv, dim=1)
+    outs = []
+    for r in rows:
+        q = x[r, : hq * hd].view(hq, hd)
+        s = torch.einsum("hd,khd->hk", q, k[: r + 1]) / hd ** 0.5
+        outs.append(torch.einsum("hk,khd->hd", torch.softmax(s, dim=-1), v[: r + 1]).reshape(-1))
+    return torch.stack(outs)
+
+
+def test_attention_long_kv_banded_order():
+    """12,288 keys x 8 kv heads (50 MB of K/V) switch the CTA order to kv-head bands (all heads' K/V exceed the L2
+    budget); spot-check query rows across the sequence and every head."""
+    n, hq, hkv = 12288, 16, 8
+    torch.manual_seed(5)
+    ld = (hq + 2 * hkv) * 128
+    qkv = torch.randn(n, ld, device="cuda").to(torch.bfloat16)
+    out = torch.full((n, hq * 128), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.call("po_op_attention", _p(qkv), ld, n, 0, hq, hkv, _p(out), hq * 128, None)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    rows = [0, 1, 127, 128, 4095, 6000, 9999, 12160, n - 1]
+    ref = ref_attention_rows(qkv, n, rows, hq, hkv)
+    got = out[rows].float()
+    err = ((got - ref).norm() / ref.norm()).item()
+    assert err < TOL, err
