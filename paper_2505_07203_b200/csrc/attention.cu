@@ -24,6 +24,7 @@
 
 namespace po {
 int set_error(int code, const char* fmt, ...);
+void keep_pool_memory();
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
                       uint32_t box_inner, uint32_t box_outer);
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
@@ -1071,6 +1072,7 @@ extern "C" int po_op_attention(const void* qkv, int64_t ld, int32_t n_total, int
   if (ld < (int64_t)(n_heads + 2 * n_kv_heads) * 128 || ld % 8)
     return po::set_error(PO_ERR_ARG, "po_op_attention: ld %lld too small or unaligned", (long long)ld);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  po::keep_pool_memory();
   const size_t ws_bytes = po::attention_workspace_bytes(n_total, q_offset, n_heads, n_kv_heads);
   void* ws = nullptr;
   if (ws_bytes && cudaMallocAsync(&ws, ws_bytes, st) != cudaSuccess)
