@@ -37,7 +37,7 @@ constexpr int BKV = 128;
 constexpr int BOX_BYTES = 128 * 64 * 2;        // one 128-row x 64-col swizzled box (16 KB)
 constexpr int TILE_BYTES = 2 * BOX_BYTES;      // 128 x 128 bf16
 constexpr int NTHREADS = 384;
-constexpr int SMEM_BYTES = 6 * TILE_BYTES + 1024 + 256 + 2048;  // + row-max exchange (ATTN_HALFROW)
+constexpr int SMEM_BYTES = 6 * TILE_BYTES + 1024 + 256;
 constexpr float RESCALE_THRESHOLD = 8.0f;      // log2 units
 #ifndef POLY_NUM
 #define POLY_NUM 3  // POLY_NUM of every POLY_DEN exp2 pairs run as the FMA-pipe polynomial (MUFU offload)
@@ -129,99 +129,8 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float&
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
-// One 128-key tile of online softmax for this thread's query row (TMEM lane): reads S, writes P (bf16,
-// packed over the first 64 columns of S), keeps (m, l). `lim` = number of visible keys in the tile
-// (keys kbase + c with c < lim); only the MASKED instantiation tests it.
-template <bool MASKED>
-__device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, int lim, float sl2, int j, float& m,
-                                             float& l) {
-  float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-  for (int c = 0; c < 4; c += 2) {
-    uint32_t v0[32], v1[32];
-    tmem_ld32(s_addr + c * 32, v0);
-    tmem_ld32(s_addr + (c + 1) * 32, v1);
-    tmem_ld_wait();
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float a0 = __uint_as_float(v0[e]), a1 = __uint_as_float(v0[e + 1]);
-      float b0 = __uint_as_float(v1[e]), b1 = __uint_as_float(v1[e + 1]);
-      if (MASKED) {
-        if (c * 32 + e >= lim) a0 = -INFINITY;
-        if (c * 32 + e + 1 >= lim) a1 = -INFINITY;
-        if ((c + 1) * 32 + e >= lim) b0 = -INFINITY;
-        if ((c + 1) * 32 + e + 1 >= lim) b1 = -INFINITY;
-      }
-      mx0 = fmaxf(mx0, fmaxf(a0, a1));
-      mx1 = fmaxf(mx1, fmaxf(b0, b1));
-    }
-  }
-  const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
-  const bool resc = m_new > m + RESCALE_THRESHOLD;
-  const float alpha = resc ? ex2_approx(m - m_new) : 1.0f;
-  if (j > 0 && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld32(o_addr + c * 32, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-      tmem_st32(o_addr + c * 32, v);
-    }
-    tmem_st_wait();
-  }
-  if (resc) {
-    l *= alpha;
-    m = m_new;
-  }
-  const float nm = -m;
-  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(nm, nm);
-  uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
-#pragma unroll
-  for (int c = 0; c < 4; c += 2) {
-    uint32_t v0[32], v1[32];
-    tmem_ld32(s_addr + c * 32, v0);
-    tmem_ld32(s_addr + (c + 1) * 32, v1);
-    tmem_ld_wait();
-    uint32_t p0[16], p1[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      float x0, x1, y0, y1;
-      up2(ffma2(pk2(__uint_as_float(v0[2 * e]), __uint_as_float(v0[2 * e + 1])), sc2, nm2), x0, x1);
-      up2(ffma2(pk2(__uint_as_float(v1[2 * e]), __uint_as_float(v1[2 * e + 1])), sc2, nm2), y0, y1);
-      if (!MASKED && (e % POLY_DEN) >= POLY_DEN - POLY_NUM) {
-        // one pair in four per chunk goes through the FMA-pipe polynomial: MUFU and FMA pipes share the load
-        exp2_poly2(x0, x1, x0, x1);
-        exp2_poly2(y0, y1, y0, y1);
-      } else {
-        x0 = ex2_approx(x0);
-        x1 = ex2_approx(x1);
-        y0 = ex2_approx(y0);
-        y1 = ex2_approx(y1);
-      }
-      if (MASKED) {
-        if (c * 32 + 2 * e >= lim) x0 = 0.f;
-        if (c * 32 + 2 * e + 1 >= lim) x1 = 0.f;
-        if ((c + 1) * 32 + 2 * e >= lim) y0 = 0.f;
-        if ((c + 1) * 32 + 2 * e + 1 >= lim) y1 = 0.f;
-      }
-      acc0 = fadd2(acc0, pk2(x0, x1));
-      acc1 = fadd2(acc1, pk2(y0, y1));
-      p0[e] = pack_bf16(x0, x1);
-      p1[e] = pack_bf16(y0, y1);
-    }
-    // P columns [16c, 16c+32) lie inside S chunks already consumed (c/2 <= c)
-    tmem_st16(s_addr + c * 16, p0);
-    tmem_st16(s_addr + (c + 1) * 16, p1);
-  }
-  float s0, s1, s2, s3;
-  up2(acc0, s0, s1);
-  up2(acc1, s2, s3);
-  l += (s0 + s1) + (s2 + s3);
-}
-
-// Single-pass variant: the whole 128-key row of S is read from TMEM once into registers (one wait), the max
+// One 128-key tile of online softmax for this thread's query row (TMEM lane). The whole row of S is read from TMEM
+// once into registers (one wait), the max
 // uses 3-input FMNMX chains, and P is written back in 32-key chunks. `on_half` runs after the first 64 keys
 // of P are stored (the caller may let the MMA warp start the first half of P.V early).
 template <bool MASKED, typename HalfFn>
@@ -298,113 +207,6 @@ __device__ __forceinline__ void softmax_tile1(uint32_t s_addr, uint32_t o_addr, 
   l += (s0 + s1) + (s2 + s3);
 }
 
-// Half-row variant (ATTN_HALFROW): thread (hh, r) owns columns [64hh, 64hh+64) of row r; warps q and q+4 share
-// TMEM lanes 32q..32q+31. The two halves agree on the tile's row max through `xch` (shared memory + a named
-// barrier) so both apply the same running max; each keeps a partial row sum. P for keys [64hh, 64hh+64) goes to
-// columns [32hh, 32hh+32) of the slot's S region (half 1 writes over S columns half 0 has already read: the
-// exchange barrier orders them).
-template <bool MASKED, typename XchFn>
-__device__ __forceinline__ void softmax_half(uint32_t s_base, uint32_t o_half, int lim, int hh, float sl2, int j,
-                                             float& m, float& l, XchFn xch) {
-  uint32_t v[64];
-  tmem_ld32(s_base + 64 * hh, *reinterpret_cast<uint32_t(*)[32]>(v));
-  tmem_ld32(s_base + 64 * hh + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-  tmem_ld_wait();
-  if (MASKED) {
-#pragma unroll
-    for (int c = 0; c < 64; ++c)
-      if (c >= lim) v[c] = __float_as_uint(-INFINITY);
-  }
-  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-  for (int e = 0; e < 64; e += 8) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(v[e + 2 * k]), __uint_as_float(v[e + 2 * k + 1])));
-  }
-  const float mloc = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-  const float m_new = fmaxf(m, fmaxf(mloc, xch(mloc)) * sl2);
-  const bool resc = m_new > m + RESCALE_THRESHOLD;
-  const float alpha = resc ? ex2_approx(m - m_new) : 1.0f;
-  if (j > 0 && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      uint32_t o[32];
-      tmem_ld32(o_half + c * 32, o);
-      tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-      tmem_st32(o_half + c * 32, o);
-    }
-    tmem_st_wait();
-  }
-  if (resc) {
-    l *= alpha;
-    m = m_new;
-  }
-  const float nm = -m;
-  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(nm, nm);
-  uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t p[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int col = 32 * c + 2 * e;
-      float x0, x1;
-      up2(ffma2(pk2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2), x0, x1);
-      if (!MASKED && (e % POLY_DEN) >= POLY_DEN - POLY_NUM) {
-        exp2_poly2(x0, x1, x0, x1);
-      } else {
-        x0 = ex2_approx(x0);
-        x1 = ex2_approx(x1);
-      }
-      if (MASKED) {
-        if (col >= lim) x0 = 0.f;
-        if (col + 1 >= lim) x1 = 0.f;
-      }
-      if (e & 1)
-        acc1 = fadd2(acc1, pk2(x0, x1));
-      else
-        acc0 = fadd2(acc0, pk2(x0, x1));
-      p[e] = pack_bf16(x0, x1);
-    }
-    tmem_st16(s_base + 32 * hh + 16 * c, p);
-  }
-  float s0, s1, s2, s3;
-  up2(acc0, s0, s1);
-  up2(acc1, s2, s3);
-  l += (s0 + s1) + (s2 + s3);
-}
-
-#ifndef ATTN_ONEPASS
-#define ATTN_ONEPASS 1
-#endif
-#ifndef ATTN_PINGPONG
-#define ATTN_PINGPONG 0
-#endif
-#ifndef ATTN_SPLITP
-#define ATTN_SPLITP 1
-#endif
-#ifndef ATTN_HALFROW
-#define ATTN_HALFROW 0
-#endif
-#if ATTN_HALFROW && ATTN_PINGPONG
-#error "ATTN_HALFROW uses named barriers 1-4; ATTN_PINGPONG is for the per-slot layout only"
-#endif
-#ifndef ATTN_ELECT
-#define ATTN_ELECT 1
-#endif
-#ifndef ATTN_SLEEPWAIT
-#define ATTN_SLEEPWAIT 0
-#endif
-// long waits of the softmax and loader warps (see mbar_wait_sleep)
-__device__ __forceinline__ void attn_wait_long(uint64_t* bar, uint32_t parity) {
-  if (ATTN_SLEEPWAIT)
-    mbar_wait_sleep(bar, parity);
-  else
-    mbar_wait(bar, parity);
-}
 
 // -DATTN_TRACE: clock64 stamps of the pipeline events of one CTA (blockIdx.x == ATTN_TRACE) for tools/attn_trace.py
 #ifdef ATTN_TRACE
@@ -433,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* s_full = bars + 7;    // [2] per head slot
   uint64_t* p_full = bars + 9;    // [2]
   uint64_t* o_final = bars + 11;  // [2]
-  uint64_t* p_half = bars + 13;   // [2] first 64 keys of P stored (ATTN_SPLITP)
+  uint64_t* p_half = bars + 13;   // [2] first 64 keys of P stored
   uint64_t* v_empty = bars + 15;  // [2] V stage free: both slots' P.V MMAs of the tile are done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
@@ -502,7 +304,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // whole 128-key row of S: 2 x 128 x 208 + 128 x 80 <= 384 x 168, the CTA's pool (asking for more blocks
   // setmaxnreg.inc forever). Issued inside each role branch so ptxas allocates each region to its own budget.
   if (warp >= 8) {
-  if (ATTN_ONEPASS) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
   if (warp == 8) {
     const uint64_t keep = l2_policy_evict_last();
     if (lane == 0) {
@@ -561,13 +363,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int cur = nxt;
       if (a.n_pool > 0) nxt = tile_slots(j + 1);
       // K of tile j+2 streams in as soon as the S MMAs of tile j are done, well before its P.V
-      attn_wait_long(&k_empty[st], ph ^ 1);
+      mbar_wait(&k_empty[st], ph ^ 1);
       TR(14, j);
       const int kr = (t0 + j) * BKV;
       if (lane == 0) mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
       __syncwarp();  // expect_tx before any lane's copies complete on the barrier
       load_kv(sK + st * TILE_BYTES, &k_full[st], kcol, a.pool_kcol + g * HD, kr, cur);
-      attn_wait_long(&v_empty[st], ph ^ 1);
+      mbar_wait(&v_empty[st], ph ^ 1);
       TR(20, j);
       if (lane == 0) mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
       __syncwarp();
@@ -575,31 +377,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp == 9) {
-    // ATTN_ELECT: the whole warp runs the issue loop (warp-uniform descriptors stay in uniform registers) and one
-    // elected lane issues the MMAs and commits; otherwise lane 0 alone runs it
-    if (ATTN_ELECT || lane == 0) {
-      const bool issuer = ATTN_ELECT ? elect_one() : true;
+    // the whole warp runs the issue loop (warp-uniform descriptors stay in uniform registers) and one elected lane
+    // issues the MMAs and commits
+    {
+      const bool issuer = elect_one();
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, 128, false, true);
       auto issue_s = [&](int i, int st) {
-#ifdef ATTN_SHALF
-        // timing experiment: S as two N=64 halves (keys 0-63 -> columns 0-63, keys 64-127 -> 64-127)
-        constexpr uint32_t idesc_h = idesc_bf16_f32(128, 64, false, false);
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * BOX_BYTES + (kk & 3) * 32;
-            if (issuer) mma_bf16_ss(tmem + i * 128 + h * 64, sdesc_kmajor_sw128(smem_u32(sQ + i * TILE_BYTES + off)),
-                        sdesc_kmajor_sw128(smem_u32(sK + st * TILE_BYTES + off + h * 64 * 128)), idesc_h, kk > 0);
-          }
-#else
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * BOX_BYTES + (kk & 3) * 32;
           if (issuer) mma_bf16_ss(tmem + i * 128, sdesc_kmajor_sw128(smem_u32(sQ + i * TILE_BYTES + off)),
                       sdesc_kmajor_sw128(smem_u32(sK + st * TILE_BYTES + off)), idesc_s, kk > 0);
         }
-#endif
         if (issuer) mma_commit(&s_full[i]);
       };
       auto issue_pv_range = [&](int i, int st, bool acc, int k0, int k1) {
@@ -609,19 +399,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (issuer) mma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, vdesc, idesc_o, (acc || kk > 0) ? 1u : 0u);
         }
       };
-      // O_i += P_i V once P_i is in TMEM; with ATTN_SPLITP the first 64 keys go as soon as their half of P is
+      // O_i += P_i V once P_i is in TMEM: the first 64 keys go as soon as their half of P is
       auto issue_pv = [&](int i, int st, bool acc, int j) {
-        if (ATTN_SPLITP) {
-          mbar_wait(&p_half[i], j & 1);
-          TR(8 + 3 * i, j);
-          tc_fence_after();
-          issue_pv_range(i, st, acc, 0, BKV / 32);
-          TR(15 + 3 * i, j);
-        }
+        mbar_wait(&p_half[i], j & 1);
+        TR(8 + 3 * i, j);
+        tc_fence_after();
+        issue_pv_range(i, st, acc, 0, BKV / 32);
+        TR(15 + 3 * i, j);
         mbar_wait(&p_full[i], j & 1);
         TR(9 + 3 * i, j);
         tc_fence_after();
-        issue_pv_range(i, st, acc, ATTN_SPLITP ? BKV / 32 : 0, BKV / 16);
+        issue_pv_range(i, st, acc, BKV / 32, BKV / 16);
         TR(16 + 3 * i, j);
       };
       mbar_wait(q_full, 0);
@@ -659,99 +447,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncwarp();
   }
   } else {
-    if (ATTN_ONEPASS) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-#if ATTN_HALFROW
-    // both softmax warpgroups work on one slot at a time (slot 0 tile j, slot 1 tile j, slot 0 tile j+1, ...), so a
-    // slot's P is ready in about half the time and the MMA chain P(j) -> P.V -> S(j+1) -> softmax stays short
-    const int hh = warp >> 2;  // column half
-    const int qd = warp & 3;   // TMEM lane quadrant
-    const int r = qd * 32 + lane;
-    const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
-    const bool packed = a.mode == MODE_PACKED;
-    const int qr = packed ? r % a.R : r;
-    float* xch = reinterpret_cast<float*>(smem + 6 * TILE_BYTES + 256);  // [2 parity][2 half][128 row]
-    const uint32_t bar_id = 1 + qd;
-    const bool tr_lane = lane == 0 && qd == 0;
-    int step = 0;
-    auto exchange = [&](float mine) -> float {
-      float* buf = xch + (step & 1) * 256;
-      buf[hh * 128 + r] = mine;
-      named_bar_sync(bar_id, 64);
-      ++step;
-      return buf[(hh ^ 1) * 128 + r];
-    };
-    float mm[2] = {-INFINITY, -INFINITY}, ll[2] = {0.f, 0.f};
-    for (int j = 0; j < n_tiles; ++j) {
-#pragma unroll 1
-      for (int i = 0; i < 2; ++i) {
-        const int my_qlo = i ? qs1 : qs0;
-        const int pos = my_qlo + qr;
-        const uint32_t s_base = tmem + lane_base + i * 128;
-        const uint32_t o_half = tmem + lane_base + 256 + i * 128 + hh * 64;
-        if (tr_lane && hh == 0) TR(4 * i, j);
-        attn_wait_long(&s_full[i], j & 1);
-        if (tr_lane && hh == 0) TR(4 * i + 1, j);
-        tc_fence_after();
-        const int kbase = (t0 + j) * BKV;
-        float mi = mm[i], li = ll[i];
-        if (kbase + BKV - 1 > my_qlo)
-          softmax_half<true>(s_base, o_half, pos - kbase + 1 - 64 * hh, hh, a.scale_log2, j, mi, li, exchange);
-        else
-          softmax_half<false>(s_base, o_half, BKV, hh, a.scale_log2, j, mi, li, exchange);
-        mm[i] = mi;
-        ll[i] = li;
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(hh == 0 ? &p_half[i] : &p_full[i]);  // keys 0-63 / 64-127 of P are in TMEM
-        if (tr_lane) TR(4 * i + 2 + hh, j);
-      }
-    }
-#pragma unroll 1
-    for (int i = 0; i < 2; ++i) {
-      attn_wait_long(&o_final[i], 0);
-      tc_fence_after();
-      const float lt = ll[i] + exchange(ll[i]);
-      const int my_qlo = i ? qs1 : qs0;
-      const int my_h = packed ? (i ? hs1 : hs0) + r / a.R : (i ? hs1 : hs0);
-      const int row = (packed && qr >= rows_slot) ? a.n_q : my_qlo - a.q_offset + qr;
-      const uint32_t o_half = tmem + lane_base + 256 + i * 128 + hh * 64;
-      if (a.splits == 1) {
-        const float inv = 1.0f / lt;
-        __nv_bfloat16* dst = a.out + (long long)row * a.ldo + my_h * HD + 64 * hh;
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          tmem_ld32(o_half + c * 32, v);
-          tmem_ld_wait();
-          if (row < a.n_q) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              d4[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv),
-                                 pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
-                                 pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv),
-                                 pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv));
-          }
-        }
-      } else {
-        const long long prow = (long long)split * a.n_q + row;
-        float4* dst = reinterpret_cast<float4*>(a.part_o + prow * (a.hq * HD) + my_h * HD + 64 * hh);
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          tmem_ld32(o_half + c * 32, v);
-          tmem_ld_wait();
-          if (row < a.n_q) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              dst[c * 8 + q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                           __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-          }
-        }
-        if (row < a.n_q && hh == 0) a.part_ml[prow * a.hq + my_h] = make_float2(mm[i], lt);
-      }
-    }
-#else
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     const int i = warp >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -767,60 +463,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool tr_lane = ((warp & 3) | lane) == 0;
     for (int j = 0; j < n_tiles; ++j) {
       if (tr_lane) TR(4 * i, j);
-      attn_wait_long(&s_full[i], j & 1);
+      mbar_wait(&s_full[i], j & 1);
       if (tr_lane) TR(4 * i + 1, j);
-      // ATTN_PINGPONG: the two slots take turns (slot 1 tile j after slot 0 tile j, slot 0 tile j+1 after
-      // slot 1 tile j), so each softmax has the MUFU to itself while the MMA runs the other slot's P.V and S
-      if (ATTN_PINGPONG) {
-        if (i == 1)
-          named_bar_sync(1, 256);
-        else if (j > 0)
-          named_bar_sync(2, 256);
-      }
       tc_fence_after();
       const int kbase = (t0 + j) * BKV;
-      // warp-uniform: only tiles crossing the diagonal of this query block pay for the mask
-#ifdef ATTN_NOSOFTMAX
-      // timing experiment only (wrong results): P is signalled ready without any softmax work
-      if (true) {
+      // the first 64 keys of P are signalled as soon as they are stored (the MMA warp starts that half of P.V)
+      auto half = [&]() {
         tmem_st_wait();
         tc_fence_before();
-        if (ATTN_SPLITP) mbar_arrive(&p_half[i]);
+        mbar_arrive(&p_half[i]);
         if (tr_lane) TR(4 * i + 2, j);
-      } else
-#endif
-      if (ATTN_ONEPASS) {
-        auto half = [&]() {
-          if (ATTN_SPLITP) {
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&p_half[i]);
-            if (tr_lane) TR(4 * i + 2, j);
-          }
-        };
-        if (kbase + BKV - 1 > my_qlo)
-          softmax_tile1<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l, half);
-        else
-          softmax_tile1<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l, half);
-      } else {
-        if (kbase + BKV - 1 > my_qlo) {
-          softmax_tile<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l);
-        } else {
-          softmax_tile<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l);
-        }
-      }
+      };
+      // warp-uniform: only tiles crossing the diagonal of this query block pay for the mask
+      if (kbase + BKV - 1 > my_qlo)
+        softmax_tile1<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l, half);
+      else
+        softmax_tile1<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l, half);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[i]);
       if (tr_lane) TR(4 * i + 3, j);
-      if (ATTN_PINGPONG) {
-        if (i == 0)
-          named_bar_arrive(1, 256);
-        else if (j + 1 < n_tiles)
-          named_bar_arrive(2, 256);
-      }
     }
-    attn_wait_long(&o_final[i], 0);
+    mbar_wait(&o_final[i], 0);
     tc_fence_after();
     const int row = (packed && qr >= rows_slot) ? a.n_q : my_qlo - a.q_offset + qr;
     if (a.splits == 1) {
@@ -860,7 +524,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if (row < a.n_q) a.part_ml[prow * a.hq + my_h] = make_float2(m, l);
     }
-#endif
   }
 
   tc_fence_before();

@@ -60,25 +60,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// try_wait with a suspend-time hint (ns): the thread sleeps in the barrier unit until the phase completes or the
-// hint expires, instead of re-polling. For warps that wait long (softmax on S, loaders on free stages) so their
-// polling does not compete with the MMA issuer's barrier traffic.
-__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t addr, uint32_t parity, uint32_t ns) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(addr), "r"(parity), "r"(ns)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 1000000) {
-  const uint32_t addr = smem_u32(bar);
-  while (!mbar_try_wait_hint(addr, parity, ns)) {
-  }
-}
 #ifdef PO_DEBUG_HANG
 __device__ __noinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);

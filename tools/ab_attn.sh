@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # A/B the attention variants built by tools/build_variant.sh: parity (test_gpu_attention) + timing per variant.
-#   tools/ab_attn.sh base twopass pp ...     (base = the in-tree library)
+#   tools/ab_attn.sh base v1 v2 ...     (base = the in-tree library)
 for v in "$@"; do
   lib=paper_2505_07203_b200/libprefillonly.so
   [ "$v" != base ] && lib=build/variants/lib_$v.so
