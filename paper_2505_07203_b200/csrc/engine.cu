@@ -6,7 +6,7 @@
 //     xn   = rmsnorm(resid) * g_attn                                       bf16 [n_miss, h]
 //     qkv[:n_c, kv]   = gather(prefix pool, cached blocks)                 bf16 K/V of the cached prefix
 //     qkv[n_c:]       = xn . Wqkv^T  (+RoPE epilogue)                      tcgen05 GEMM
-//     pool[admitted]  = qkv[admitted rows, kv]                             prefix-pool admission
+//     pool[admitted]  = K/V of the admitted rows (stored by the QKV epilogue) prefix-pool admission
 //     ctx  = causal GQA attention(qkv, q_offset = n_c)                     full length, tcgen05 FA
 //     resid += ctx . Wo^T                                                  residual epilogue, in place
 //     for chunk of rows:                                                   hybrid: MLP chunked
@@ -74,7 +74,7 @@ struct po_engine {
   // per-request device staging
   uint32_t* d_tokens = nullptr;
   int* d_slots = nullptr;
-  int2* d_admit = nullptr;
+  int* d_kvslot = nullptr;  // per 16-token block: admission slot in the prefix pool, or -1
   int* d_allowed = nullptr;
   float* d_logits = nullptr;
   float* d_probs = nullptr;
@@ -82,7 +82,7 @@ struct po_engine {
   // pinned host staging
   uint32_t* h_tokens = nullptr;
   int* h_slots = nullptr;
-  int2* h_admit = nullptr;
+  int* h_kvslot = nullptr;
   int* h_allowed = nullptr;
   float* h_logits = nullptr;
   float* h_probs = nullptr;
@@ -175,7 +175,7 @@ int po_free(po_engine* e) {
   for (void* p : e->allocs) cudaFree(p);
   cudaFreeHost(e->h_tokens);
   cudaFreeHost(e->h_slots);
-  cudaFreeHost(e->h_admit);
+  cudaFreeHost(e->h_kvslot);
   cudaFreeHost(e->h_allowed);
   cudaFreeHost(e->h_logits);
   cudaFreeHost(e->h_probs);
@@ -292,14 +292,14 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
   const long long max_blocks = T / c.block_tokens + 1;
   if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_slots, (size_t)max_blocks * 4, &e->arena_bytes) ||
-      dalloc(e, &e->d_admit, (size_t)max_blocks * 8, &e->arena_bytes) ||
+      dalloc(e, &e->d_kvslot, (size_t)max_blocks * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_allowed, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_logits, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_probs, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_argmax, 16, &e->arena_bytes))
     return fail(PO_ERR_CUDA, "staging allocation failed");
   if (halloc(&e->h_tokens, (size_t)T * 4) || halloc(&e->h_slots, (size_t)max_blocks * 4) ||
-      halloc(&e->h_admit, (size_t)max_blocks * 8) || halloc(&e->h_allowed, (size_t)c.vocab * 4) ||
+      halloc(&e->h_kvslot, (size_t)max_blocks * 4) || halloc(&e->h_allowed, (size_t)c.vocab * 4) ||
       halloc(&e->h_logits, (size_t)c.vocab * 4) || halloc(&e->h_probs, (size_t)c.vocab * 4) ||
       halloc(&e->h_argmax, 16))
     return fail(PO_ERR_CUDA, "pinned host allocation failed");
@@ -437,6 +437,7 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
   const int n_c = n_cached < n ? n_cached : n - 1;
   const int cached_blocks = (n_c + bt - 1) / bt;
   int n_admit = 0;
+  for (int b = 0; b <= n / bt; ++b) e->h_kvslot[b] = -1;
   for (int b = 0; b < n_blocks; ++b) {
     const int slot = pool_block_ids[b];
     if (b < n_cached / bt) {
@@ -445,7 +446,8 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
       if (b < cached_blocks) e->h_slots[b] = slot;
     } else if (slot >= 0) {
       if (slot >= e->pool_blocks) return set_error(PO_ERR_POOL, "po_prefill: admit slot %d out of range", slot);
-      e->h_admit[n_admit++] = make_int2(b, slot);
+      e->h_kvslot[b] = slot;
+      ++n_admit;
     }
   }
   *n_admit_out = n_admit;
@@ -521,7 +523,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     }
   };
   if (cached_blocks) cudaMemcpyAsync(e->d_slots, e->h_slots, (size_t)cached_blocks * 4, cudaMemcpyHostToDevice, s);
-  if (n_admit) cudaMemcpyAsync(e->d_admit, e->h_admit, (size_t)n_admit * 8, cudaMemcpyHostToDevice, s);
+  if (n_admit) cudaMemcpyAsync(e->d_kvslot, e->h_kvslot, (size_t)(n / bt + 1) * 4, cudaMemcpyHostToDevice, s);
 
   // RMSNorm is folded across the GEMMs (GemmArgs): producers (embedding, residual epilogues) write
   // xg = bf16(resid . gamma_next) and per-segment sums of squares; consumers scale rows by 1/rms.
@@ -555,17 +557,15 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
     g.split_ws = e->gemm_ws;
     g.bias = ly.bqkv;
+    if (n_admit) {  // suffix-block admission: the QKV epilogue also stores the admitted rows' K/V into the pool
+      g.kv_slot = e->d_kvslot; g.kv_pool = e->pool; g.pool_layers = L; g.pool_layer = l;
+      g.kv_col0 = kv_col0; g.kv_dim = kvd;
+    }
     norm_in(g, e->ss_attn);
     mark(KC_QKV, true);
     rc |= gemm(e->map_xg, e->xg, h, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
     ++launches;
-    if (n_admit) {
-      mark(KC_SCATTER, true);
-      po::launch_kv_scatter(e->qkv, qkvc, kv_col0, e->d_admit, n_admit, l, L, bt, kvd, e->pool, s);
-      mark(KC_SCATTER, false);
-      ++launches;
-    }
     // the last layer only needs the final row's output (the LM head reads nothing else); its K/V rows
     // were computed (and admitted to the pool) above
     const bool last_only = c.last_row_only && l == L - 1 && n_miss > 1;

@@ -54,6 +54,25 @@ __device__ __forceinline__ float row_inv_rms(const GemmArgs& a, int row) {
   return rsqrtf(s / a.norm_dim + a.norm_eps);
 }
 
+// Prefix-pool row (offset so that column index col addresses it) of output row `row` when its block is admitted
+// and the column block [hcol, hcol + 128) holds K or V; null otherwise (see GemmArgs::kv_slot).
+__device__ __forceinline__ __nv_bfloat16* pool_row(const GemmArgs& a, int row, int hcol) {
+  if (!a.kv_pool || hcol < a.kv_col0) return nullptr;
+  const int pos = a.pos_offset + row;
+  const int slot = a.kv_slot[pos >> 4];
+  if (slot < 0) return nullptr;
+  return a.kv_pool + (((long long)slot * a.pool_layers + a.pool_layer) * 16 + (pos & 15)) * a.kv_dim - a.kv_col0;
+}
+__device__ __forceinline__ void store_bf16_32(__nv_bfloat16* dst, const uint32_t (&r)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    d[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1])),
+                      pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3])),
+                      pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5])),
+                      pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
+}
+
 template <int EPI>
 __device__ __forceinline__ float epilogue_chunk(const GemmArgs& a, int row, int col0, const uint32_t (&r)[32],
                                                 float sc = 1.0f) {
@@ -177,6 +196,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
           }
           epilogue_chunk<EPI_BF16>(args, row, hcol + half * 32, x1);
           epilogue_chunk<EPI_BF16>(args, row, hcol + 64 + half * 32, x2);
+          if (__nv_bfloat16* prow = pool_row(args, row, hcol)) {
+            store_bf16_32(prow + hcol + half * 32, x1);
+            store_bf16_32(prow + hcol + 64 + half * 32, x2);
+          }
         }
       }
     }
@@ -557,15 +580,20 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
         const float4 x1 = acc;
         const float2 c0 = cs[0], c1 = cs[1], c2 = cs[2], c3 = cs[3];
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col;
-        *reinterpret_cast<uint2*>(o) =
-            make_uint2(pack_bf16(x1.x * c0.x - x2.x * c0.y, x1.y * c1.x - x2.y * c1.y),
-                       pack_bf16(x1.z * c2.x - x2.z * c2.y, x1.w * c3.x - x2.w * c3.y));
-        *reinterpret_cast<uint2*>(o + 64) =
-            make_uint2(pack_bf16(x2.x * c0.x + x1.x * c0.y, x2.y * c1.x + x1.y * c1.y),
-                       pack_bf16(x2.z * c2.x + x1.z * c2.y, x2.w * c3.x + x1.w * c3.y));
+        const uint2 lo = make_uint2(pack_bf16(x1.x * c0.x - x2.x * c0.y, x1.y * c1.x - x2.y * c1.y),
+                                    pack_bf16(x1.z * c2.x - x2.z * c2.y, x1.w * c3.x - x2.w * c3.y));
+        const uint2 hi = make_uint2(pack_bf16(x2.x * c0.x + x1.x * c0.y, x2.y * c1.x + x1.y * c1.y),
+                                    pack_bf16(x2.z * c2.x + x1.z * c2.y, x2.w * c3.x + x1.w * c3.y));
+        *reinterpret_cast<uint2*>(o) = lo;
+        *reinterpret_cast<uint2*>(o + 64) = hi;
+        if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) {
+          *reinterpret_cast<uint2*>(prow + col) = lo;
+          *reinterpret_cast<uint2*>(prow + col + 64) = hi;
+        }
       } else if (col >= a.rope_cols) {
-        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
-            make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+        const uint2 v = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) = v;
+        if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) *reinterpret_cast<uint2*>(prow + col) = v;
       }
     }
   }

@@ -41,6 +41,12 @@ struct GemmArgs {
   int k_splits;
   int kb_per_split;
   float* split_ws;
+  // EPI_QKV_ROPE prefix-pool admission (replaces a separate scatter pass): rows whose 16-token block b (absolute
+  // position / 16) has kv_slot[b] >= 0 also store their K/V columns [kv_col0, kv_col0 + kv_dim) into
+  // kv_pool[(slot * pool_layers + pool_layer) * 16 + position % 16][kv_dim].
+  const int* kv_slot;
+  __nv_bfloat16* kv_pool;
+  int pool_layers, pool_layer, kv_col0, kv_dim;
 };
 
 struct GemmPlan {

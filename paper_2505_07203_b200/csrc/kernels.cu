@@ -1,5 +1,5 @@
 // Memory-bound kernels of the PrefillOnly forward: embedding gather, RMSNorm, prefix-pool KV
-// gather/scatter, allowed-row LM head; plus the counter-based on-device weight init.
+// gather (A/B mode only), allowed-row LM head; plus the counter-based on-device weight init.
 #include "kernels.cuh"
 #include <cfloat>
 
@@ -121,35 +121,11 @@ __global__ void kv_gather_kernel(const __nv_bfloat16* __restrict__ pool, const i
     reinterpret_cast<uint4*>(qkv + r * ld + col0)[q] = src[q];
   }
 }
-__global__ void kv_scatter_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int col0,
-                                  const int2* __restrict__ admit, int n_admit, int layer, int num_layers, int bt,
-                                  int kv_dim, __nv_bfloat16* __restrict__ pool) {
-  pdl_wait();
-  pdl_trigger();
-  const int vec = kv_dim / 8;
-  const long long total = (long long)n_admit * bt * vec;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long rb = i / vec;
-    const int q = static_cast<int>(i - rb * vec);
-    const int a = static_cast<int>(rb / bt), t = static_cast<int>(rb % bt);
-    const int2 bs = admit[a];  // (block index within request, pool slot)
-    const long long row = (long long)bs.x * bt + t;
-    uint4* dst = reinterpret_cast<uint4*>(pool + (((long long)bs.y * num_layers + layer) * bt + t) * kv_dim);
-    dst[q] = reinterpret_cast<const uint4*>(qkv + row * ld + col0)[q];
-  }
-}
 void launch_kv_gather(const __nv_bfloat16* pool, const int* slots, int n_rows, int layer, int num_layers,
                       int block_tokens, int kv_dim, __nv_bfloat16* qkv, long long ld, int col0, cudaStream_t s) {
   if (n_rows <= 0) return;
   launch_pdl(kv_gather_kernel, dim3(148 * 8), dim3(256), 0, s, pool, slots, n_rows, layer, num_layers, block_tokens,
              kv_dim, qkv, ld, col0);
-}
-void launch_kv_scatter(const __nv_bfloat16* qkv, long long ld, int col0, const int2* admit, int n_admit, int layer,
-                       int num_layers, int block_tokens, int kv_dim, __nv_bfloat16* pool, cudaStream_t s) {
-  if (n_admit <= 0) return;
-  launch_pdl(kv_scatter_kernel, dim3(148 * 8), dim3(256), 0, s, qkv, ld, col0, admit, n_admit, layer, num_layers,
-             block_tokens, kv_dim, pool);
 }
 
 // ------------------------------------------------------------------ allowed-row LM head

@@ -29,12 +29,10 @@ void launch_init_bias(float* dst, long long n, uint64_t seed, uint32_t tid, cuda
 // 128-column segment seg (the first layer's folded RMSNorm input, see GemmArgs)
 void launch_embed_norm(const uint32_t* tokens, int n, const __nv_bfloat16* embed, int vocab, int hidden,
                        const float* gamma, float* resid, __nv_bfloat16* xg, float* ss, cudaStream_t s);
-// Prefix pool <-> layer qkv buffer. Pool layout: [slot][layer][block_tokens][kv_dim] bf16.
+// Prefix pool -> layer qkv buffer (only with PO_POOL_DIRECT=0; admission is stored by the QKV GEMM epilogue).
+// Pool layout: [slot][layer][block_tokens][kv_dim] bf16.
 void launch_kv_gather(const __nv_bfloat16* pool, const int* slots, int n_rows, int layer, int num_layers,
                       int block_tokens, int kv_dim, __nv_bfloat16* qkv, long long ld, int col0, cudaStream_t s);
-void launch_kv_scatter(const __nv_bfloat16* qkv, long long ld, int col0, const int2* admit /*(block, slot)*/,
-                       int n_admit, int layer, int num_layers, int block_tokens, int kv_dim, __nv_bfloat16* pool,
-                       cudaStream_t s);
 // Last-row final norm + allowed-row LM head + restricted softmax + argmax.
 void launch_lm_head(const float* resid_row, int hidden, const float* gamma, float eps, const __nv_bfloat16* w,
                     const int* allowed, int n_allowed, float* logits, float* probs, int* argmax, cudaStream_t s);

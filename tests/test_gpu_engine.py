@@ -183,3 +183,22 @@ def test_pool_direct_straddling_tiles_match_oracle(tiny_engine, n_cached):
     warm = tiny_engine.prefill(req, YES_NO, n_cached=n_cached, pool_block_ids=ids)
     assert warm.n_cached == n_cached
     check_against_oracle(TINY, warm, req, YES_NO, 42)
+
+
+@pytest.mark.parametrize("model", [TINY, SMALL], ids=["tiny", "small-splitk"])
+def test_short_suffix_admission_feeds_later_hits(model):
+    """A prefix hit with a short miss suffix admits its suffix blocks from the QKV epilogue (the pair GEMM for the
+    tiny model, the split-K reduce for `small`); a later request whose cached prefix covers those blocks must match
+    the oracle."""
+    slots = list(range(300, 300 + 80))
+    allowed = [a % model.vocab for a in YES_NO]
+    with Engine(model, seed=42, max_tokens=2048, chunk=1024, pool_blocks=512) as eng:
+        a_toks = tokens_for(31, 640)
+        eng.prefill(a_toks, allowed, n_cached=0, pool_block_ids=slots[:40])       # A: admit 40 blocks
+        b_toks = np.concatenate([a_toks, tokens_for(32, 160)])                     # B: hit + 160-token suffix
+        b = eng.prefill(b_toks, allowed, n_cached=640, pool_block_ids=slots[:50])  # admits blocks 40..49
+        check_against_oracle(model, b, b_toks, allowed, 42)
+        c_toks = np.concatenate([b_toks, tokens_for(33, 48)])                      # C: cached through B's suffix
+        c = eng.prefill(c_toks, allowed, n_cached=800, pool_block_ids=slots[:50] + [-1] * 3)
+        assert c.n_cached == 800
+        check_against_oracle(model, c, c_toks, allowed, 42)
