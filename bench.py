@@ -217,6 +217,16 @@ def executed_flops_per_class(M, n: int, last_row_only: bool) -> dict:
             "attention": 4.0 * h * pairs}
 
 
+def hbm_bytes_per_class(M, n: int, n_allowed: int) -> dict:
+    """Algorithmic DRAM bytes per request of the memory-bound kernel classes (cold n-token request)."""
+    h = M.hidden
+    # embedding rows (bf16) in; fp32 residual, bf16 folded-norm input and per-128-column sums of squares out
+    embed = n * h * 2 + n * h * 4 + n * h * 2 + n * (h // 128) * 4
+    # last residual row + final norm gamma + the allowed LM-head rows in; logits / probs / argmax out
+    lm_head = h * 4 + h * 4 + n_allowed * h * 2 + n_allowed * 8 + 4
+    return {"embed": embed, "lm_head": lm_head}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -331,6 +341,7 @@ def main():
     peaks, peak_src = load_peaks()
     sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     cls_flops = executed_flops_per_class(M, n, eng.last_row_only)
+    cls_bytes = hbm_bytes_per_class(M, n, len(ALLOWED))
     total_ms = sum(v[0] for v in prof.values())
     traffic = {}
     tpath = ROOT / "profiles" / "ncu_traffic.json"
@@ -343,8 +354,13 @@ def main():
             ach = cls_flops[name] * K / (ms / 1e3) / 1e12
             entry.update({"bound": "tensor", "achieved": ach, "unit": "TFLOP/s", "peak": sustained,
                           "frac": ach / sustained, "frac_of_burst": ach / peaks["bf16_tflops"]})
+        elif name in cls_bytes and ms > 0:
+            gbs = cls_bytes[name] * K / (ms / 1e3) / 1e9
+            entry.update({"bound": "hbm" if name != "lm_head" else "latency", "achieved": gbs, "unit": "GB/s",
+                          "peak": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
+                          "bytes_per_request": cls_bytes[name]})
         by_kernel[name] = entry
-    top = max((k for k in by_kernel if "achieved" in by_kernel[k]), key=lambda k: by_kernel[k]["share"])
+    top = max((k for k in by_kernel if by_kernel[k].get("unit") == "TFLOP/s"), key=lambda k: by_kernel[k]["share"])
     t = by_kernel[top]
     roofline = {"kernel": top, "bound": "tensor", "achieved": t["achieved"], "peak": sustained, "unit": "TFLOP/s",
                 "frac": t["frac"], "traffic": traffic.get(top),
