@@ -19,8 +19,8 @@ request with a Yes/No allowed list, cold prefix cache. One STEP = one request th
   qps_at_slo  post-recommendation 20k workload (40 users x 50 requests, shared profiles) under Poisson
           arrivals, calibrated SRJF + prefix pool, sticky routing over N GPUs: largest rate whose p99
           latency meets the SLO. The event loop is the reference's (serving.simulate, virtual clock); every
-          distinct request shape (n, n_cached) it meets is run for real on the GPU once and its measured
-          device time reused (serving.MeasuredServiceFn).
+          request of the saturation run is executed for real on the GPU in serving order and its measured
+          device time reused by the rate sweep (serving.ReplayServiceFn).
   cpu_baseline  the CPU port of the reference path (oracle/llama_ref.py, numpy f64) timed on this host on a
           bounded sample (one Llama-8B layer at 1,024 tokens), extrapolated by the FLOP formula.
 """
@@ -448,29 +448,30 @@ def prefix_hit_roofline(eng, M, n, peaks):
 def qps_at_slo(eng, M, world, rank, slo, dist):
     """Calibrated-SRJF serving of the post-recommendation 20k workload over `world` GPU replicas.
 
-    Virtual-clock event loop with the reference's semantics (serving.simulate); every distinct request shape
-    (n_input, n_cached) the loop encounters is run for real on this GPU once (MeasuredServiceFn) and its
-    device time reused. Rank 0 runs the loop for all replicas (identical GPUs, sticky user routing).
+    Virtual-clock event loop with the reference's semantics (serving.simulate); every request of the saturation
+    run executes for real on this GPU in serving order (ReplayServiceFn) and the rate sweep reuses those device
+    times. Rank 0 runs the loop for all replicas (identical GPUs, sticky user routing).
     """
     from paper_2505_07203_b200 import workload as wl
     from paper_2505_07203_b200.scheduling import Policy
-    from paper_2505_07203_b200.serving import MeasuredServiceFn, qps_at_slo as pick, simulate, sweep_rates
+    from paper_2505_07203_b200.serving import ReplayServiceFn, qps_at_slo as pick, simulate, sweep_rates
 
     if rank != 0:
         return None
     trace = wl.gen_post_recommendation(0, wl.POSTREC_20K)
     capacity = min(eng.capacity_tokens, 16 * eng.pool_blocks)
-    svc = MeasuredServiceFn(eng, ALLOWED)
+    svc = ReplayServiceFn(eng, ALLOWED)
     t0 = time.perf_counter()
     run = lambda tr, pol=None: simulate(tr, world, pol or Policy.srjf_calibrated(), capacity, svc)  # noqa: E731
-    sat = run(wl.zero_arrivals(trace)).throughput
+    sat = run(wl.zero_arrivals(trace)).throughput  # every request runs for real here, in serving order
+    svc.recording = False
     rates = [sat * m for m in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0)]
     res = sweep_rates(trace, rates, seed=0, run=run)
     fifo = sweep_rates(trace, rates, seed=0, run=lambda tr: run(tr, Policy.fifo()))
     best = pick(res, slo)
     rep = dict(res)[best] if best else None
-    hits = sorted(v[0] for (n, nc), v in svc.memo.items() if nc > 0)
-    colds = sorted(v[0] for (n, nc), v in svc.memo.items() if nc == 0)
+    hits = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc > 0)
+    colds = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc == 0)
     return {
         "value": best, "unit": "requests/s", "slo_p99_s": slo, "n_gpus": world,
         "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
@@ -482,8 +483,9 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         "workload": "post-recommendation 40 users x 50 requests, profiles 19,850 +- 3,000 tokens + 150-token "
                     "suffix, Poisson arrivals (user sessions contiguous), Yes/No allowed ids",
         "method": f"virtual-clock serving loop with the reference's event semantics (calibrated SRJF, prefix pool of "
-                  f"{capacity} tokens per GPU, sticky routing over {world} replica(s)); each of the "
-                  f"{svc.forwards} distinct (n, n_cached) shapes ran as a real forward on GPU 0 "
+                  f"{capacity} tokens per GPU, sticky routing over {world} replica(s)); every request of the "
+                  f"saturation run executed for real on GPU 0 in serving order and its device time reused by the "
+                  f"rate sweep (shapes the sweep meets beyond those: one forward each); {svc.forwards} real forwards "
                   f"({time.perf_counter() - t0:.1f} s wall)",
         "measured_service_s": {"cold_median": statistics.median(colds) if colds else None,
                                "prefix_hit_median": statistics.median(hits) if hits else None},

@@ -83,3 +83,35 @@ def test_service_fn_receives_pool_plan():
     (a_id, a_nc, a_ids), (d_id, d_nc, d_ids) = seen[0], seen[1]
     assert (a_id, d_id, a_nc, d_nc) == (0, 3, 0, 1024)
     assert d_ids[:64] == a_ids[:64] and len(d_ids) == 2944 // 16
+
+
+def test_replay_service_fn_records_each_request_once_and_reuses():
+    """ReplayServiceFn: the saturation run executes every request (in serving order) and records it; later runs
+    reuse the recorded (request, n_cached) times and measure only unseen shapes."""
+    from paper_2505_07203_b200 import workload as wl
+    from paper_2505_07203_b200.scheduling import Policy
+    from paper_2505_07203_b200.serving import ReplayServiceFn, simulate
+
+    class Eng:
+        def __init__(self):
+            self.calls = 0
+
+        def prefill(self, tokens, allowed, n_cached=0, pool_block_ids=None):
+            self.calls += 1
+
+            class R:
+                service_s = 1e-3 * (len(tokens) - n_cached) / 1000 + 1e-4 * self.calls
+                token = allowed[0]
+            return R()
+
+    trace = wl.gen_post_recommendation(0, wl.POSTREC_20K)
+    trace = type(trace)(trace.name, trace.seed, trace.requests[:120])
+    eng = Eng()
+    svc = ReplayServiceFn(eng, [1, 2])
+    rep0 = simulate(wl.zero_arrivals(trace), 1, Policy.srjf_calibrated(), 400_000, svc)
+    assert eng.calls == len(trace.requests) == len(svc.by_request)  # every request ran for real, once
+    svc.recording = False
+    calls = eng.calls
+    rep1 = simulate(wl.zero_arrivals(trace), 1, Policy.srjf_calibrated(), 400_000, svc)
+    assert eng.calls == calls  # same order and cache state: all reused
+    assert rep1.p99_latency == rep0.p99_latency
