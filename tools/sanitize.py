@@ -22,11 +22,16 @@ for n, off, hq, hkv in ((300, 0, 4, 2), (600, 560, 8, 2), (300, 0, 5, 1)):
     qkv = torch.randn(n, ld, device="cuda").to(torch.bfloat16)
     out = torch.empty(n - off, hq * 128, dtype=torch.bfloat16, device="cuda")
     _lib.call("po_op_attention", p(qkv), ld, n, off, hq, hkv, p(out), hq * 128, None)
-# engine: cold, admission, prefix hit
-with Engine(TINY, seed=1, max_tokens=1024, chunk=256, pool_blocks=64) as e:
-    t = np.random.default_rng(0).integers(0, 2**32, size=600, dtype=np.uint32)
-    slots = list(range(600 // 16))
-    e.prefill(t, [1, 2], 0, slots)
-    e.prefill(t, [1, 2], 512, slots)
+# engine: cold with admission, then prefix hits read straight from the pool (tile-aligned and straddling prefixes),
+# for the tiny model (pair-GEMM epilogue admission) and a wider one (split-K reduce admission)
+from paper_2505_07203_b200.config import ModelConfig
+SMALL = ModelConfig("small", 2, 1024, 8, 2, 128, 2816, 4096)
+for model in (TINY, SMALL):
+    with Engine(model, seed=1, max_tokens=1024, chunk=256, pool_blocks=128) as e:
+        t = np.random.default_rng(0).integers(0, 2**32, size=800, dtype=np.uint32)
+        slots = list(range(800 // 16))
+        e.prefill(t[:600], [1, 2], 0, slots[:37])
+        e.prefill(t[:600], [1, 2], 512, slots[:37])
+        e.prefill(t, [1, 2], 592, slots)  # straddling tile + suffix admission
 torch.cuda.synchronize()
 print("sanitize workload done")
