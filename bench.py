@@ -349,6 +349,8 @@ def main():
         traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch", {})
     by_kernel = {}
     for name, (ms, cnt) in prof.items():
+        if cnt == 0:
+            continue  # kernel classes this forward does not launch (norm folded into GEMMs, gather in A/B mode only)
         entry = {"ms_per_step": ms / K, "launches_per_step": cnt / K, "share": ms / total_ms if total_ms else 0.0}
         if name in cls_flops and ms > 0:
             ach = cls_flops[name] * K / (ms / 1e3) / 1e12
