@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  if (threadIdx.x == 0) TR(21, 0);
 
   // heaviest (longest causal extent) units first. Slot i of this CTA: head hs_i (first head of the kv group
   // when packed), first query position qs_i; rows_slot query rows per head in the slot.
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TR(21, 1);
   pdl_wait();     // qkv of this layer (QKV GEMM, pool gather) complete
   pdl_trigger();
   // registers move from the loader/MMA warpgroup (warps 8-11) to the two softmax warpgroups, which hold a
@@ -524,6 +526,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if (row < a.n_q) a.part_ml[prow * a.hq + my_h] = make_float2(m, l);
     }
+    if (tr_lane) TR(22 + i, 0);
   }
 
   tc_fence_before();
