@@ -18,6 +18,7 @@
 // kept stale until it grows by > 8 (log2 units), so O is rescaled in TMEM only rarely; the final
 // normalisation divides by the matching running sum, so the result is exact softmax.
 #include "sm100.cuh"
+#include "attention.cuh"
 #include "../../include/prefillonly.h"
 #include <cmath>
 #include <cstdlib>
@@ -71,15 +72,6 @@ struct AttnArgs {
   int pool_layer, pool_layers;  // map_pool block index = slot * pool_layers + pool_layer
   int pool_kcol, pool_vcol;     // column of this launch's K / V head 0 within a pool row
   int kv_band;                  // MODE_HEADS CTA order: kv heads per band (0 = all heads interleaved)
-};
-
-// Pool-direct key source of one attention launch (see AttnArgs): the prefix pool [num_blocks][num_layers][16][kv_dim]
-// bf16 and the request's per-block slots.
-struct AttnPool {
-  const void* base;
-  const int* slots;
-  int n_rows;  // cached key rows (multiple of 16) read from the pool
-  int num_blocks, num_layers, layer, kv_dim, block_tokens;
 };
 
 // Slot layouts. HEADS: two query heads of one GQA group over the same 128-row query block (K/V shared).

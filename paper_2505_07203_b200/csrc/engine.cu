@@ -17,6 +17,7 @@
 #include "../../include/prefillonly.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "attention.cuh"
 #include <cmath>
 #include <cstring>
 #include <cstdio>
@@ -27,15 +28,6 @@
 
 namespace po {
 int set_error(int code, const char* fmt, ...);
-struct AttnPool {
-  const void* base;
-  const int* slots;
-  int n_rows;
-  int num_blocks, num_layers, layer, kv_dim, block_tokens;
-};
-int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
-                  cudaStream_t stream, void* workspace, size_t workspace_bytes, const AttnPool* pool);
-size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv);
 }  // namespace po
 
 struct po_engine {
