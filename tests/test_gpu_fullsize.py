@@ -1,0 +1,95 @@
+"""BASELINE-size properties on the GPU: Llama-3.1-8B at 20k and 128k tokens.
+
+The float64 oracle cannot run these sizes in test time (one 20k-token layer is ~1e13 FLOP), so these checks use
+properties that do not depend on size:
+* determinism (bit-identical logits on a repeat);
+* a normalised restricted softmax;
+* a prefix hit served from the pool agrees with the cold forward of the same prompt, within the bf16 logit
+  tolerance of test_gpu_engine (split-K / split-KV change the summation order, so not bit for bit);
+* the MLP chunk size does not change the result (per-row work: bit-exact, ps/numerics.py hybrid == full).
+Exact parity against the oracle is established at the smaller sizes in test_gpu_engine.py.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2505_07203_b200.config import LLAMA_3_1_8B
+from paper_2505_07203_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_ATOL = 2e-2
+LOGIT_RTOL = 2e-2
+YES_NO = [9642, 2822]
+MANY = YES_NO + list(range(0, 128_256, 997))  # a longer allowed list across the whole vocab
+
+
+def tokens_for(seed: int, n: int) -> np.ndarray:
+    return np.random.default_rng([seed, 0, 0]).integers(0, 2 ** 32, size=n, dtype=np.uint32)
+
+
+def close(a, b):
+    return bool((np.abs(a - b) <= LOGIT_ATOL + LOGIT_RTOL * np.abs(b)).all())
+
+
+def normalised(res):
+    return np.isfinite(res.logits).all() and abs(float(res.probs.sum()) - 1.0) < 1e-5 and res.probs.min() >= 0
+
+
+@pytest.fixture(scope="module")
+def llama20k():
+    with Engine(LLAMA_3_1_8B, seed=0, max_tokens=20_480, pool_blocks=1_300) as e:
+        yield e
+
+
+def test_llama8b_20k_cold_is_deterministic_and_normalised(llama20k):
+    toks = tokens_for(0, 20_000)
+    a = llama20k.prefill(toks, MANY)
+    b = llama20k.prefill(toks, MANY)
+    assert normalised(a)
+    assert np.array_equal(a.logits, b.logits) and a.index == b.index
+    assert a.logits[a.index] == a.logits.max()
+    # the allowed list's order does not matter: the same logits come back permuted
+    perm = list(reversed(MANY))
+    c = llama20k.prefill(toks, perm)
+    assert np.array_equal(c.logits[::-1], a.logits)
+
+
+def test_llama8b_20k_prefix_hit_agrees_with_cold(llama20k):
+    n, bt = 20_000, 16
+    toks = tokens_for(1, n)
+    slots = list(range(n // bt))
+    cold = llama20k.prefill(toks, YES_NO, 0, slots)  # cold, admitting all 1,250 blocks into the pool
+    n_c = (n - 160) // bt * bt
+    hit = llama20k.prefill(toks, YES_NO, n_c, slots)
+    print("20k cold", cold.logits, "hit", hit.logits, "service s", cold.service_s, hit.service_s)
+    assert hit.n_cached == n_c and normalised(hit)
+    assert close(hit.logits, cold.logits), (hit.logits, cold.logits)
+    assert hit.service_s < cold.service_s / 10
+    # a different suffix behind the same cached prefix is a different request: it must not reuse stale rows
+    other = toks.copy()
+    other[n_c:] = tokens_for(2, n - n_c)
+    hit2 = llama20k.prefill(other, YES_NO, n_c, slots[: n_c // bt] + [-1] * (n // bt - n_c // bt))
+    cold2 = llama20k.prefill(other, YES_NO)
+    assert close(hit2.logits, cold2.logits), (hit2.logits, cold2.logits)
+
+
+def test_llama8b_chunk_size_does_not_change_result():
+    toks = tokens_for(3, 12_000)
+    outs = []
+    for chunk in (8192, 2048):
+        with Engine(LLAMA_3_1_8B, seed=0, max_tokens=12_288, chunk=chunk, pool_blocks=16) as e:
+            outs.append(e.prefill(toks, YES_NO).logits)
+    assert np.array_equal(outs[0], outs[1]), outs
+
+
+def test_llama8b_128k_single_request_and_hit():
+    n, bt = 131_072, 16
+    toks = tokens_for(4, n)
+    with Engine(LLAMA_3_1_8B, seed=0, max_tokens=n, pool_blocks=n // bt + 8) as e:
+        slots = list(range(n // bt))
+        cold = e.prefill(toks, YES_NO, 0, slots)
+        hit = e.prefill(toks, YES_NO, n - 160, slots)
+    print("128k cold", cold.logits, "hit", hit.logits, "service s", cold.service_s, hit.service_s)
+    assert normalised(cold) and normalised(hit)
+    assert close(hit.logits, cold.logits), (hit.logits, cold.logits)
