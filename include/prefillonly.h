@@ -50,6 +50,21 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
                int64_t ldr, int32_t M, int32_t N, int32_t K, int32_t epi, const void* rope_table,
                int32_t pos_offset, int32_t rope_cols, void* stream);
 
+/* FP8 (W8A8 E4M3) variant of po_op_gemm for the paper's FP8-weight presets (ps/presets/qwen-32b-fp8.preset:1-16,
+ * ps/presets/llama-3.3-70b-fp8.preset:1-15; tcgen05 kind::f8f6f4). A [M,K] and B [N,K] are E4M3 bytes (lda/ldb
+ * in bytes), a_scale [M] / b_scale [N] fp32 dequantisation scales: acc[m,n] * a_scale[m] * b_scale[n] feeds the
+ * same epilogues as po_op_gemm. Requires N % 256 == 0 and K % 128 == 0. */
+int po_op_gemm_fp8(const void* A, int64_t lda, const float* a_scale, const void* B, int64_t ldb,
+                   const float* b_scale, void* out, int64_t ldo, float* resid, int64_t ldr, int32_t M, int32_t N,
+                   int32_t K, int32_t epi, const void* rope_table, int32_t pos_offset, int32_t rope_cols,
+                   void* stream);
+
+/* Per-row dynamic E4M3 quantisation of a bf16 [rows, cols] matrix (activations before an FP8 GEMM, or weight
+ * rows = output channels): scale[r] = amax_r / 448, q[r,c] = e4m3_satfinite_rn(x[r,c] * (448 / amax_r)).
+ * cols % 16 == 0, ldx % 8 == 0, ldq % 16 == 0 (elements / bytes). */
+int po_op_quantize_e4m3(const void* x, int64_t ldx, int32_t rows, int32_t cols, void* q, int64_t ldq, float* scale,
+                        void* stream);
+
 /* Causal GQA attention over one layer's qkv buffer (bf16 [n_total, ld]: Q | K | V columns, head_dim 128).
  * Rows [0, q_offset) are cached-prefix rows that act only as keys; the output ctx (bf16 [n_total-q_offset,
  * ldo]) holds the n_total-q_offset query rows. Replaces _attention (ps/numerics.py:132-146) generalised to

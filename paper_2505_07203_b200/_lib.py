@@ -58,6 +58,9 @@ SIGNATURES = {
     "po_load_weight": (_I32, [_VP, _I32, _I32, _VP, _I64]),
     "po_op_attention": (_I32, [_VP, _I64, _I32, _I32, _I32, _I32, _VP, _I64, _VP]),
     "po_op_gemm": (_I32, [_VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP, _I32, _I32, _VP]),
+    "po_op_gemm_fp8": (_I32, [_VP, _I64, _VP, _VP, _I64, _VP, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP, _I32,
+                              _I32, _VP]),
+    "po_op_quantize_e4m3": (_I32, [_VP, _I64, _I32, _I32, _VP, _I64, _VP, _VP]),
 }
 
 

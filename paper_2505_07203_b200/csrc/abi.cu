@@ -67,4 +67,53 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
   return PO_OK;
 }
 
+int po_op_gemm_fp8(const void* A, int64_t lda, const float* a_scale, const void* B, int64_t ldb,
+                   const float* b_scale, void* out, int64_t ldo, float* resid, int64_t ldr, int32_t M, int32_t N,
+                   int32_t K, int32_t epi, const void* rope_table, int32_t pos_offset, int32_t rope_cols,
+                   void* stream) {
+  if (!A || !B || !a_scale || !b_scale) return po::set_error(PO_ERR_ARG, "po_op_gemm_fp8: null operand or scale");
+  if (M <= 0 || N <= 0 || N % 256 || K <= 0 || K % 128)
+    return po::set_error(PO_ERR_ARG, "po_op_gemm_fp8: need M>0, N%%256==0, K%%128==0 (got %d,%d,%d)", M, N, K);
+  if (epi == PO_EPI_RESID_F32 ? !resid : !out) return po::set_error(PO_ERR_ARG, "po_op_gemm_fp8: null output");
+  if (epi == PO_EPI_QKV_ROPE && !rope_table) return po::set_error(PO_ERR_ARG, "po_op_gemm_fp8: null rope table");
+  CUtensorMap map_a, map_b;
+  if (po::make_tmap_a_f8(&map_a, A, lda, M, K) || po::make_tmap_a_f8(&map_b, B, ldb, N, K))
+    return po::set_error(PO_ERR_CUDA, "po_op_gemm_fp8: tensor map encode failed");
+  po::GemmArgs args{};
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.out = out;
+  args.ldo = ldo;
+  args.resid = resid;
+  args.ldr = ldr;
+  args.rope = static_cast<const float2*>(rope_table);
+  args.pos_offset = pos_offset;
+  args.rope_cols = rope_cols;
+  args.a_scale = a_scale;
+  args.b_scale = b_scale;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  po::keep_pool_memory();
+  const size_t ws = po::gemm_split_ws_bytes_f8(M, N, K);
+  if (ws && cudaMallocAsync(reinterpret_cast<void**>(&args.split_ws), ws, st) != cudaSuccess)
+    return po::set_error(PO_ERR_CUDA, "po_op_gemm_fp8: split-K workspace allocation failed");
+  int rc = po::gemm_launch_pair_f8(map_a, map_b, epi, args, st);
+  if (args.split_ws) cudaFreeAsync(args.split_ws, st);
+  if (rc) return po::set_error(PO_ERR_CUDA, "po_op_gemm_fp8: launch failed (%d): %s", rc,
+                               cudaGetErrorString(cudaGetLastError()));
+  return PO_OK;
+}
+
+int po_op_quantize_e4m3(const void* x, int64_t ldx, int32_t rows, int32_t cols, void* q, int64_t ldq, float* scale,
+                        void* stream) {
+  if (!x || !q || !scale) return po::set_error(PO_ERR_ARG, "po_op_quantize_e4m3: null pointer");
+  if (rows < 0 || cols <= 0 || cols % 16 || ldx % 8 || ldq % 16 || ldx < cols || ldq < cols)
+    return po::set_error(PO_ERR_ARG, "po_op_quantize_e4m3: need cols%%16==0, ldx%%8==0, ldq%%16==0 (got %d,%lld,%lld)",
+                         cols, (long long)ldx, (long long)ldq);
+  int rc = po::quantize_rows_e4m3(static_cast<const __nv_bfloat16*>(x), ldx, rows, cols, static_cast<uint8_t*>(q), ldq,
+                                  scale, static_cast<cudaStream_t>(stream));
+  if (rc) return po::set_error(PO_ERR_CUDA, "po_op_quantize_e4m3: launch failed (%d)", rc);
+  return PO_OK;
+}
+
 }  // extern "C"

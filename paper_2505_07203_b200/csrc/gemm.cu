@@ -7,6 +7,7 @@
 //   warps 4..7  epilogue: tcgen05.ld 32 rows x 32 columns per warp, fused op, global store
 // Pipelines: smem full/empty ring (TMA <-> MMA) and TMEM full/empty pair (MMA <-> epilogue).
 #include "gemm.cuh"
+#include <cuda_fp8.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
@@ -139,9 +140,26 @@ __device__ __forceinline__ float epilogue_chunk(const GemmArgs& a, int row, int 
   return sq;
 }
 
+// FP8: dequantise 32 accumulator columns [col0, col0 + 32) of this row: acc * a_scale[row] * b_scale[col]
+template <bool F8>
+__device__ __forceinline__ void dequant32(const GemmArgs& a, float as, int col0, uint32_t (&r)[32]) {
+  if constexpr (F8) {
+    const float4* b4 = reinterpret_cast<const float4*>(a.b_scale + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = __ldg(b4 + q);
+      r[4 * q + 0] = __float_as_uint(__uint_as_float(r[4 * q + 0]) * as * b.x);
+      r[4 * q + 1] = __float_as_uint(__uint_as_float(r[4 * q + 1]) * as * b.y);
+      r[4 * q + 2] = __float_as_uint(__uint_as_float(r[4 * q + 2]) * as * b.z);
+      r[4 * q + 3] = __float_as_uint(__uint_as_float(r[4 * q + 3]) * as * b.w);
+    }
+  }
+}
+
 // Epilogue of one 128-row x 256-column accumulator (this thread: TMEM lane = output row `row`).
-template <int EPI, int BNT = BN>
+template <int EPI, int BNT = BN, bool F8 = false>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t taddr, int row, int nb, int ksp, int t) {
+  const float as = (F8 && row < args.M) ? args.a_scale[row] : 0.f;
   if (ksp > 1) {
     // split-K partial: raw fp32 tile into the workspace slice of this split
     GemmArgs pa = args;
@@ -168,6 +186,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
         tmem_ld32(taddr + h * 128 + half * 32, x1);
         tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
         tmem_ld_wait();
+        dequant32<F8>(args, as, hcol + half * 32, x1);
+        dequant32<F8>(args, as, hcol + 64 + half * 32, x2);
         if (args.ss_in) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -210,6 +230,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
+      dequant32<F8>(args, as, nb * BNT + c, r);
       if (row < args.M) sq[c >> 7] += epilogue_chunk<EPI>(args, row, nb * BNT + c, r);
     }
     if (args.ss_out && row < args.M) {
@@ -223,6 +244,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
+      dequant32<F8>(args, as, nb * BNT + c, r);
       if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BNT + c, r, sc);
     }
   }
@@ -367,10 +389,12 @@ struct Pair {
 };
 }  // namespace
 
-template <int EPI, int BNT>
+// F8: E4M3 operands (kind::f8f6f4); a k-block is still one 128-byte row per operand row (128 elements instead of 64)
+template <int EPI, int BNT, bool F8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const GemmArgs args) {
+  constexpr int KE = F8 ? 2 * BK : BK;  // k elements per k-block
   constexpr int STAGES2 = Pair<BNT>::STAGES;
   constexpr int B_HALF = Pair<BNT>::B_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -392,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int num_n = args.N / BNT;
   const int ksp = args.k_splits > 1 ? args.k_splits : 1;
   const int num_tiles = num_m * num_n * ksp;
-  const int nk_total = args.K / BK;
+  const int nk_total = args.K / KE;
   const int kbps = ksp > 1 ? args.kb_per_split : nk_total;
 
   if (warp == 0 && lane == 0) {
@@ -432,8 +456,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * Pair<BNT>::STAGE);
           const uint32_t fb = full0 + s * 8;
-          tma_load_2d_pair(sA + s * HALF_BYTES, &map_a, fb, kb * BK, args.a_row0 + mb * 2 * BM + rank * BM);
-          tma_load_2d_pair(sB + s * B_HALF, &map_b, fb, kb * BK, nb * BNT + rank * (BNT / 2));
+          tma_load_2d_pair(sA + s * HALF_BYTES, &map_a, fb, kb * KE, args.a_row0 + mb * 2 * BM + rank * BM);
+          tma_load_2d_pair(sB + s * B_HALF, &map_b, fb, kb * KE, nb * BNT + rank * (BNT / 2));
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
       }
@@ -441,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BNT);
+      constexpr uint32_t idesc = F8 ? idesc_e4m3_f32(2 * BM, BNT) : idesc_bf16_f32(2 * BM, BNT);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -459,8 +483,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           const uint64_t adesc = sdesc_kmajor_sw128(smem_u32(sA + s * HALF_BYTES));
           const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sB + s * B_HALF));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {  // 4 MMAs of 32 bytes of K each (K16 bf16 or K32 e4m3)
+            if constexpr (F8)
+              mma_f8_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            else
+              mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
           mma_commit_pair(&empty_bar[s], 0x3);
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
@@ -481,7 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row = mb * 2 * BM + rank * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BNT;
-      epilogue_tile<EPI, BNT>(args, taddr, row, nb, ksp, t);
+      epilogue_tile<EPI, BNT, F8>(args, taddr, row, nb, ksp, t);
       tc_fence_before();
       named_bar_sync(1, 128);
       if (threadIdx.x == 128) mbar_arrive_cluster(tempty0 + acc * 8);
@@ -516,6 +544,17 @@ __device__ __forceinline__ float4 split_sum(const float* p, size_t slice, int sp
   return acc;
 }
 
+// FP8 split-K: dequantise a summed 4-column group (same order as dequant32: (acc * a_scale) * b_scale)
+__device__ __forceinline__ void dq4(const GemmArgs& a, int row, int col, float4& v) {
+  if (!a.b_scale) return;
+  const float as = a.a_scale[row];
+  const float4 b = *reinterpret_cast<const float4*>(a.b_scale + col);
+  v.x = v.x * as * b.x;
+  v.y = v.y * as * b.y;
+  v.z = v.z * as * b.z;
+  v.w = v.w * as * b.w;
+}
+
 template <int EPI>
 __global__ void splitk_reduce_kernel(const GemmArgs a) {
   pdl_wait();
@@ -529,6 +568,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
     const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
     const float* p = a.split_ws + (size_t)row * a.N + col;
     float4 acc = split_sum(p, slice, a.k_splits);
+    dq4(a, row, col, acc);
     float sc = 1.0f;
     if constexpr (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
       if (a.ss_in) sc = row_inv_rms(a, row);
@@ -559,6 +599,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       const int grp = col / 32, w = col % 32;
       if (w < 16) {
         float4 up = split_sum(p + 16, slice, a.k_splits);
+        dq4(a, row, col + 16, up);
         up.x *= sc; up.y *= sc; up.z *= sc; up.w *= sc;
         const int oc = grp * 16 + w;
         *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
@@ -572,6 +613,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       }
       if (col < a.rope_cols && head_col < 64) {
         float4 x2 = split_sum(p + 64, slice, a.k_splits);
+        dq4(a, row, col + 64, x2);
         x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
         if (a.bias) {
           x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
@@ -704,12 +746,12 @@ size_t gemm_split_ws_bytes(int M, int N, int K) {
   return smax > 1 ? (size_t)smax * M * N * sizeof(float) : 0;
 }
 
-template <int EPI, int BNT>
+template <int EPI, int BNT, bool F8 = false>
 static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, const GemmArgs& in,
                          cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gemm2_kernel<EPI, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Pair<BNT>::SMEM);
+    cudaFuncSetAttribute(gemm2_kernel<EPI, BNT, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Pair<BNT>::SMEM);
     configured = true;
   }
   GemmArgs args = in;
@@ -717,7 +759,7 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
   const int tiles_mn = ((args.M + 2 * BM - 1) / (2 * BM)) * (args.N / BNT);
   if (args.split_ws) {
     // pair tiles: split K while fewer than SM-pairs/2 tiles exist (small-M prefix-hit GEMMs)
-    const int nk = args.K / BK;
+    const int nk = args.K / (F8 ? 2 * BK : BK);
     int s = 1;
     const int pairs = num_sms() / 2;
     if (tiles_mn * 2 <= pairs && nk >= 16) {
@@ -733,7 +775,7 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
   }
   const int tiles = tiles_mn * args.k_splits;
   const int npairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  launch_pdl(gemm2_kernel<EPI, BNT>, dim3(2 * npairs), dim3(NUM_THREADS), Pair<BNT>::SMEM, stream, map_a, map_b2,
+  launch_pdl(gemm2_kernel<EPI, BNT, F8>, dim3(2 * npairs), dim3(NUM_THREADS), Pair<BNT>::SMEM, stream, map_a, map_b2,
              args);
   if (args.k_splits > 1) {
     const long long total = (long long)args.M * (args.N / 4);
@@ -802,6 +844,100 @@ int gemm_launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, int ep
     case EPI_F32: return launch_pair<EPI_F32>(map_a, map_b2, map_b3, args, stream);
     default: return -3;
   }
+}
+
+// ------------------------------------------------------------------ FP8 (E4M3, W8A8)
+int make_tmap_a_f8(CUtensorMap* map, const void* A, long long lda, long long rows, int K) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)lda};
+  cuuint32_t box[2] = {2 * BK, BM};  // 128 bytes x 128 rows, the bf16 box geometry
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(A), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+size_t gemm_split_ws_bytes_f8(int M, int N, int K) {
+  const int tiles_mn = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  const int nk = K / (2 * BK);
+  int s = 1;
+  if (tiles_mn * 2 <= num_sms() / 2 && nk >= 16) {
+    s = (num_sms() / 2) / tiles_mn;
+    s = s < nk / 8 ? s : nk / 8;
+    s = s > 1 ? s : 1;
+  }
+  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
+}
+
+int gemm_launch_pair_f8(const CUtensorMap& map_a, const CUtensorMap& map_b2, int epi, const GemmArgs& args,
+                        cudaStream_t stream) {
+  if (args.M <= 0) return 0;
+  if (args.N % BN || args.K % (2 * BK) || !args.a_scale || !args.b_scale) return -3;
+  switch (epi) {
+    case EPI_BF16: return launch_pair_t<EPI_BF16, 256, true>(map_a, map_b2, args, stream);
+    case EPI_RESID_F32: return launch_pair_t<EPI_RESID_F32, 256, true>(map_a, map_b2, args, stream);
+    case EPI_SILU_MUL: return launch_pair_t<EPI_SILU_MUL, 256, true>(map_a, map_b2, args, stream);
+    case EPI_QKV_ROPE: return launch_pair_t<EPI_QKV_ROPE, 256, true>(map_a, map_b2, args, stream);
+    case EPI_F32: return launch_pair_t<EPI_F32, 256, true>(map_a, map_b2, args, stream);
+    default: return -3;
+  }
+}
+
+// One CTA per row: amax over the row (8 bf16 per 16-byte load), then e4m3 = satfinite_rn(x * 448 / amax).
+__global__ void __launch_bounds__(256) quantize_rows_kernel(const __nv_bfloat16* __restrict__ x, long long ldx, int cols,
+                                                            uint8_t* __restrict__ q, long long ldq,
+                                                            float* __restrict__ scale) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(x + (long long)row * ldx);
+  const int nv = cols / 8;
+  float amax = 0.f;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const uint4 v = src[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+      amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = red[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) amax = fmaxf(amax, red[k]);
+  const float inv = amax > 0.f ? 448.f / amax : 0.f;
+  if (threadIdx.x == 0) scale[row] = amax / 448.f;
+  uint2* dst = reinterpret_cast<uint2*>(q + (long long)row * ldq);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const uint4 v = src[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[2];
+#pragma unroll
+    for (int k = 0; k < 4; k += 2) {
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k + 1]));
+      const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(f0.x * inv, f0.y * inv), __NV_SATFINITE, __NV_E4M3);
+      const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(f1.x * inv, f1.y * inv), __NV_SATFINITE, __NV_E4M3);
+      o[k / 2] = lo | (hi << 16);
+    }
+    dst[i] = make_uint2(o[0], o[1]);
+  }
+}
+
+int quantize_rows_e4m3(const __nv_bfloat16* x, long long ldx, int rows, int cols, uint8_t* q, long long ldq,
+                       float* scale, cudaStream_t stream) {
+  if (rows <= 0) return 0;
+  if (cols % 16 || ldx % 8 || ldq % 16) return -3;
+  launch_pdl(quantize_rows_kernel, dim3(rows), dim3(256), 0, stream, x, ldx, cols, q, ldq, scale);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
 int gemm_launch(const CUtensorMap& map_a, const CUtensorMap& map_b, int epi, const GemmArgs& args,

@@ -47,6 +47,10 @@ struct GemmArgs {
   const int* kv_slot;
   __nv_bfloat16* kv_pool;
   int pool_layers, pool_layer, kv_col0, kv_dim;
+  // FP8 (W8A8, E4M3 operands; gemm_launch_pair_f8 only): acc[m,n] is dequantised as acc * a_scale[m] * b_scale[n]
+  // (per-row activation scale from quantize_rows_e4m3, per-output-channel weight scale) before the epilogue.
+  const float* a_scale;
+  const float* b_scale;
 };
 
 struct GemmPlan {
@@ -78,6 +82,22 @@ int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, 
 bool gemm_use_pair(int M);  // pair kernel for M > 128 unless PO_GEMM_1CTA=1
 int make_tmap_b(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int num_sms();
+
+// ---- FP8 (E4M3) path: the paper's FP8-weight presets (ps/presets/qwen-32b-fp8.preset, llama-3.3-70b-fp8.preset)
+// as W8A8 on tcgen05 kind::f8f6f4. Operands are row-major [rows, K] bytes; K % 128 == 0 (one 128-byte row per
+// k-block, the same swizzle and stage geometry as bf16 with BK = 64).
+// 128-row (A / pair B half) box map over an E4M3 [rows, K] matrix.
+int make_tmap_a_f8(CUtensorMap* map, const void* A, long long lda, long long rows, int K);
+// D = dequant(A) . dequant(B)^T with the fused epilogues of gemm_launch_pair (2-CTA pair kernel for every M;
+// split-K for short M when args.split_ws is set). args.a_scale / args.b_scale are required.
+int gemm_launch_pair_f8(const CUtensorMap& map_a, const CUtensorMap& map_b2, int epi, const GemmArgs& args,
+                        cudaStream_t stream);
+// Workspace bytes of an FP8 launch of this shape (0 = no split).
+size_t gemm_split_ws_bytes_f8(int M, int N, int K);
+// Per-row dynamic quantisation: scale[r] = amax(|x[r,:]|) / 448, q[r,c] = e4m3_rn_satfinite(x[r,c] * (448 / amax))
+// (scale 0 and q = 0 for an all-zero row). One CTA per row; cols % 16 == 0.
+int quantize_rows_e4m3(const __nv_bfloat16* x, long long ldx, int rows, int cols, uint8_t* q, long long ldq,
+                       float* scale, cudaStream_t stream);
 
 
 }  // namespace po
