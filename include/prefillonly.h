@@ -99,6 +99,9 @@ typedef struct po_model_cfg {
   int32_t last_row_only;     /* 1: in the last layer run attention/O/MLP for the final row only (exact:    */
                              /*    only that row reaches the LM head); 0: every row through every layer  */
   int32_t qkv_bias;          /* 1: q/k/v projections carry a bias (Qwen2), added before RoPE               */
+  int32_t weight_fp8;        /* 1: layer weights stored E4M3 with per-output-channel scales (the FP8 presets,   */
+                             /*    ps/presets/qwen-32b-fp8.preset:1-16); GEMMs run W8A8 (kind::f8f6f4) with   */
+                             /*    per-row dynamic activation scales. Embedding and LM head stay bf16.       */
 } po_model_cfg;
 
 typedef struct po_engine po_engine;

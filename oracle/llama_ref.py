@@ -15,6 +15,11 @@ What it restates (numpy, float64 arithmetic):
 
 bf16-faithful: values are rounded to bf16 at the same storage points as the kernels (the folded-RMSNorm GEMM
 input bf16(x . gamma), roped q/k, v, attention output, SiLU.mul output, final hidden); accumulation is float64.
+
+FP8 (cfg.weight_fp8, the reference's FP8 presets ps/presets/qwen-32b-fp8.preset:1-16): layer weights are the bf16
+init quantised per output row to E4M3, and every layer GEMM input is quantised per row the same way
+(`quantize_rows`, mirroring csrc/gemm.cu quantize_rows_kernel: fp32 amax, inv = 448 / amax, e4m3 RNE satfinite of
+x * inv, scale = amax / 448); products are then taken in float64 on the dequantised values.
 """
 
 from __future__ import annotations
@@ -38,6 +43,32 @@ def bf16_round(x) -> np.ndarray:
     bits = a.view(np.uint32).astype(np.uint64)
     rounded = ((bits + np.uint64(0x7FFF) + ((bits >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
     return rounded.astype(np.uint32).view(np.float32).reshape(a.shape)
+
+
+def e4m3_round(x) -> np.ndarray:
+    """Round to the nearest E4M3 value (OCP FP8, ties to even, saturating at +-448); float64 in, float64 out."""
+    a = np.asarray(x, dtype=np.float64)
+    m = np.minimum(np.abs(a), 448.0)
+    _, ex = np.frexp(m)                      # m = f * 2^ex, f in [0.5, 1)
+    e = np.maximum(ex - 1, -6)               # binade exponent; subnormals share the 2^-6 binade's spacing
+    step = np.ldexp(1.0, e - 3)              # 3 mantissa bits
+    return np.sign(a) * np.rint(m / step) * step
+
+
+def quantize_rows(x) -> tuple[np.ndarray, np.ndarray]:
+    """Per-row E4M3 quantisation as the kernel does it in fp32: returns (codes as float64, scale float32)."""
+    xf = np.asarray(x, dtype=np.float32)
+    amax = np.abs(xf).max(axis=-1).astype(np.float32)
+    with np.errstate(divide="ignore"):
+        inv = np.where(amax > 0, np.float32(448.0) / amax, np.float32(0.0)).astype(np.float32)
+    y = (xf * inv[..., None]).astype(np.float32)
+    return e4m3_round(y), (amax / np.float32(448.0)).astype(np.float32)
+
+
+def fp8_dequant_rows(x) -> np.ndarray:
+    """quantize_rows then dequantise (codes * scale) in float64: the value an FP8 GEMM multiplies."""
+    q, sc = quantize_rows(x)
+    return q * sc.astype(np.float64)[..., None]
 
 
 def splitmix64(x: np.ndarray) -> np.ndarray:
@@ -106,6 +137,7 @@ class Cfg:
     rope_high_freq_factor: float = 4.0
     rope_original_max_pos: int = 8192
     qkv_bias: bool = False
+    weight_fp8: bool = False
 
     @classmethod
     def from_model(cls, m) -> "Cfg":
@@ -135,6 +167,9 @@ def make_weights(cfg: Cfg, seed: int) -> dict:
         })
         if cfg.qkv_bias:
             w["layers"][-1]["bqkv"] = init_bias(seed, layer_tid(l, K_QKV_BIAS), (cfg.n_heads + 2 * cfg.n_kv_heads) * hd)
+        if cfg.weight_fp8:  # E4M3 per output row (rows are independent, so q/k/v and gate/up quantise separately)
+            for name in ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down"):
+                w["layers"][-1][name] = fp8_dequant_rows(w["layers"][-1][name])
     return w
 
 
@@ -273,8 +308,11 @@ def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_
         ang = np.arange(n, dtype=np.float64)[:, None] * inv[None, :]
         cos, sin = np.cos(ang), np.sin(ang)
     x = w["embed"][toks.astype(np.int64)].astype(np.float64)
+    # FP8: every layer GEMM input is quantised per row (after its bf16 rounding), the weights already are
+    Q = fp8_dequant_rows if getattr(cfg, "weight_fp8", False) else (lambda a: a)
     for lw in w["layers"]:
         xg, inv = folded_norm(x, lw["attn_norm"], cfg.rms_eps, R)
+        xg = Q(xg)
         q = inv * (xg @ lw["wq"].T.astype(np.float64))
         k = inv * (xg @ lw["wk"].T.astype(np.float64))
         v = inv * (xg @ lw["wv"].T.astype(np.float64))
@@ -285,12 +323,13 @@ def llama_forward(cfg: Cfg, w: dict, tokens, allowed, n_cached: int = 0, return_
         q = R(apply_rope(q, cos, sin))
         k = R(apply_rope(k, cos, sin))
         v = R(v)
-        ctx = R(causal_attention(q, k, v)).reshape(n, hq * hd)
+        ctx = Q(R(causal_attention(q, k, v)).reshape(n, hq * hd))
         x = x + ctx @ lw["wo"].T.astype(np.float64)
         xg2, inv2 = folded_norm(x, lw["mlp_norm"], cfg.rms_eps, R)
+        xg2 = Q(xg2)
         g = inv2 * (xg2 @ lw["w_gate"].T.astype(np.float64))
         u = inv2 * (xg2 @ lw["w_up"].T.astype(np.float64))
-        act = R(silu(g) * u)
+        act = Q(R(silu(g) * u))
         x = x + act @ lw["w_down"].T.astype(np.float64)
     h_last = rmsnorm(x[-1:], w["final_norm"], cfg.rms_eps, R)[0]
     alw = np.asarray(allowed, dtype=np.int64)

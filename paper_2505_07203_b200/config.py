@@ -33,6 +33,7 @@ class ModelConfig:
     rope_high_freq_factor: float = 4.0
     rope_original_max_pos: int = 8192
     qkv_bias: bool = False  # Qwen2-style q/k/v projection bias
+    weight_fp8: bool = False  # E4M3 layer weights + per-channel scales, W8A8 GEMMs (the reference's FP8 presets)
 
     @property
     def kv_bytes_per_token(self) -> tuple[int, int]:
@@ -45,6 +46,10 @@ class ModelConfig:
         h, i = self.hidden, self.intermediate
         qkv = (self.n_heads + 2 * self.n_kv_heads) * self.head_dim * h
         o = self.n_heads * self.head_dim * h
+        if self.weight_fp8:  # E4M3 matrices + fp32 per-output-channel scales; embedding, LM head, norms bf16
+            qkv_rows = (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+            per_layer = qkv + o + 3 * h * i + 4 * (qkv_rows + h + 2 * i + h) + 2 * 2 * h
+            return self.num_layers * per_layer + 2 * (2 * self.vocab * h + h)
         per_layer = qkv + o + 3 * h * i + 2 * h
         return 2 * (self.num_layers * per_layer + 2 * self.vocab * h + h)
 
@@ -77,7 +82,13 @@ TINY = ModelConfig("tiny", 2, 256, 2, 1, 128, 1024, 32_000)
 QWEN_2_5_32B = ModelConfig("qwen-2.5-32b", 64, 5120, 40, 8, 128, 27648, 152_064, rms_eps=1e-6,
                            rope_theta=1_000_000.0, rope_scaling=0, qkv_bias=True)
 
-PRESETS = {c.name: c for c in (TINY, LLAMA_3_1_8B, QWEN_2_5_32B)}
+# The reference's FP8-weight presets (ps/presets/qwen-32b-fp8.preset:1-16, ps/presets/llama-3.3-70b-fp8.preset:1-15):
+# the same shapes with E4M3 layer weights. Llama-3.3-70B: meta-llama/Llama-3.3-70B-Instruct config.json.
+QWEN_2_5_32B_FP8 = replace(QWEN_2_5_32B, name="qwen-2.5-32b-fp8", weight_fp8=True)
+LLAMA_3_3_70B_FP8 = ModelConfig("llama-3.3-70b-fp8", 80, 8192, 64, 8, 128, 28672, 128_256, weight_fp8=True)
+TINY_FP8 = replace(TINY, name="tiny-fp8", weight_fp8=True)
+
+PRESETS = {c.name: c for c in (TINY, LLAMA_3_1_8B, QWEN_2_5_32B, QWEN_2_5_32B_FP8, LLAMA_3_3_70B_FP8, TINY_FP8)}
 
 
 def get_preset(name: str) -> ModelConfig:
@@ -112,6 +123,7 @@ class PoModelCfg(ctypes.Structure):
         ("pool_mem_fraction", ctypes.c_double),
         ("last_row_only", ctypes.c_int32),
         ("qkv_bias", ctypes.c_int32),
+        ("weight_fp8", ctypes.c_int32),
     ]
 
 
@@ -120,6 +132,7 @@ def to_c_cfg(model: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK, bl
     d = asdict(model)
     d.pop("name")
     d["qkv_bias"] = int(d["qkv_bias"])
+    d["weight_fp8"] = int(d["weight_fp8"])
     return PoModelCfg(**d, max_tokens=max_tokens, chunk=chunk, block_tokens=block_tokens, pool_blocks=pool_blocks,
                       pool_mem_fraction=pool_mem_fraction, last_row_only=int(last_row_only))
 
@@ -141,4 +154,4 @@ def executed_flops(model: ModelConfig, n: int, n_cached: int = 0, last_row_only:
 
 
 __all__ = ["ModelConfig", "PoModelCfg", "to_c_cfg", "get_preset", "PRESETS", "TINY", "LLAMA_3_1_8B",
-           "QWEN_2_5_32B", "DEFAULT_CHUNK", "BLOCK_TOKENS", "replace"]
+           "QWEN_2_5_32B", "QWEN_2_5_32B_FP8", "LLAMA_3_3_70B_FP8", "TINY_FP8", "DEFAULT_CHUNK", "BLOCK_TOKENS", "replace"]

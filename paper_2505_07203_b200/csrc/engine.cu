@@ -47,6 +47,10 @@ struct po_engine {
     CUtensorMap map_qkv, map_o, map_gu, map_down;      // 256-row boxes (1-CTA kernel)
     CUtensorMap map2_qkv, map2_o, map2_gu, map2_down;  // 128-row boxes (2-CTA pair kernel)
     CUtensorMap map3_qkv, map3_o, map3_gu, map3_down;  // 64-row boxes (narrow pair tiles, small M)
+    // weight_fp8: E4M3 copies [rows, K] with fp32 per-row (output-channel) scales replace the bf16 matrices
+    uint8_t *q_qkv = nullptr, *q_o = nullptr, *q_gu = nullptr, *q_down = nullptr;
+    float *s_qkv = nullptr, *s_o = nullptr, *s_gu = nullptr, *s_down = nullptr;
+    CUtensorMap f8_qkv, f8_o, f8_gu, f8_down;  // 128-row boxes of 128 bytes (pair kernel)
   };
   std::vector<Layer> layers;
   // arena
@@ -63,6 +67,10 @@ struct po_engine {
   void* attn_ws = nullptr;  // split-KV partials for short-query (prefix-hit) requests
   size_t attn_ws_bytes = 0;
   CUtensorMap map_xn, map_ctx, map_act, map_xg;
+  // weight_fp8: per-row E4M3 copies of the GEMM inputs (xg, ctx, act) and their dequantisation scales
+  uint8_t *xg8 = nullptr, *ctx8 = nullptr, *act8 = nullptr;
+  float *xg_s = nullptr, *ctx_s = nullptr, *act_s = nullptr;
+  CUtensorMap map_xg8, map_ctx8, map_act8;
   // per-request device staging
   uint32_t* d_tokens = nullptr;
   int* d_slots = nullptr;
@@ -97,6 +105,7 @@ struct po_engine {
   int kv_dim() const { return 2 * cfg.n_kv_heads * cfg.head_dim; }
   int ctx_cols() const { return cfg.n_heads * cfg.head_dim; }
   int64_t block_bytes() const { return (int64_t)cfg.num_layers * cfg.block_tokens * kv_dim() * 2; }
+  bool fp8() const { return cfg.weight_fp8 != 0; }
 };
 
 namespace {
@@ -215,39 +224,83 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
   po::launch_init_bf16(e->lm_head, c.vocab, h, seed, TID_LM_HEAD, 0, fan_scale(h), po::INIT_PLAIN, s);
   po::launch_init_norm(e->final_norm, h, seed, TID_FINAL_NORM, s);
   e->layers.resize(L);
-  for (int l = 0; l < L; ++l) {
+  // weight_fp8: each bf16 matrix is generated into a scratch buffer (not counted as weights) and quantised per output
+  // row into its E4M3 copy, so the random init is the bf16 model's, rounded once more
+  const bool f8 = e->fp8();
+  __nv_bfloat16* wtmp = nullptr;
+  if (f8) {
+    const size_t most = std::max(std::max((size_t)qkvc * h, (size_t)h * ctxc), std::max((size_t)2 * I * h, (size_t)h * I));
+    if (cudaMalloc(&wtmp, most * 2) != cudaSuccess) return fail(PO_ERR_CUDA, "weight scratch allocation failed");
+  }
+  auto quant = [&](int rows, int cols, uint8_t* q, float* sc) {
+    return po::quantize_rows_e4m3(wtmp, cols, rows, cols, q, cols, sc, s);
+  };
+  int wrc = 0;
+  for (int l = 0; l < L && !wrc; ++l) {
     auto& ly = e->layers[l];
-    if (dalloc(e, &ly.wqkv, (size_t)qkvc * h * 2, &e->weight_bytes) ||
-        dalloc(e, &ly.wo, (size_t)h * ctxc * 2, &e->weight_bytes) ||
-        dalloc(e, &ly.wgu, (size_t)2 * I * h * 2, &e->weight_bytes) ||
-        dalloc(e, &ly.wdown, (size_t)h * I * 2, &e->weight_bytes) ||
-        dalloc(e, &ly.attn_norm, (size_t)h * 4, &e->weight_bytes) ||
-        dalloc(e, &ly.mlp_norm, (size_t)h * 4, &e->weight_bytes))
+    if (!f8 && (dalloc(e, &ly.wqkv, (size_t)qkvc * h * 2, &e->weight_bytes) ||
+                dalloc(e, &ly.wo, (size_t)h * ctxc * 2, &e->weight_bytes) ||
+                dalloc(e, &ly.wgu, (size_t)2 * I * h * 2, &e->weight_bytes) ||
+                dalloc(e, &ly.wdown, (size_t)h * I * 2, &e->weight_bytes)))
+      wrc = -1;
+    if (f8 && (dalloc(e, &ly.q_qkv, (size_t)qkvc * h, &e->weight_bytes) ||
+               dalloc(e, &ly.s_qkv, (size_t)qkvc * 4, &e->weight_bytes) ||
+               dalloc(e, &ly.q_o, (size_t)h * ctxc, &e->weight_bytes) ||
+               dalloc(e, &ly.s_o, (size_t)h * 4, &e->weight_bytes) ||
+               dalloc(e, &ly.q_gu, (size_t)2 * I * h, &e->weight_bytes) ||
+               dalloc(e, &ly.s_gu, (size_t)2 * I * 4, &e->weight_bytes) ||
+               dalloc(e, &ly.q_down, (size_t)h * I, &e->weight_bytes) ||
+               dalloc(e, &ly.s_down, (size_t)h * 4, &e->weight_bytes)))
+      wrc = -1;
+    if (wrc || dalloc(e, &ly.attn_norm, (size_t)h * 4, &e->weight_bytes) ||
+        dalloc(e, &ly.mlp_norm, (size_t)h * 4, &e->weight_bytes)) {
+      cudaFree(wtmp);
       return fail(PO_ERR_CUDA, "weight allocation failed");
+    }
     const int qrows = c.n_heads * c.head_dim, kvrows = c.n_kv_heads * c.head_dim;
-    po::launch_init_bf16(ly.wqkv, qrows, h, seed, layer_tid(l, K_Q), 0, fan_scale(h), po::INIT_PLAIN, s);
-    po::launch_init_bf16(ly.wqkv + (size_t)qrows * h, kvrows, h, seed, layer_tid(l, K_K), 0, fan_scale(h),
+    __nv_bfloat16* wqkv = f8 ? wtmp : ly.wqkv;
+    po::launch_init_bf16(wqkv, qrows, h, seed, layer_tid(l, K_Q), 0, fan_scale(h), po::INIT_PLAIN, s);
+    po::launch_init_bf16(wqkv + (size_t)qrows * h, kvrows, h, seed, layer_tid(l, K_K), 0, fan_scale(h),
                          po::INIT_PLAIN, s);
-    po::launch_init_bf16(ly.wqkv + (size_t)(qrows + kvrows) * h, kvrows, h, seed, layer_tid(l, K_V), 0, fan_scale(h),
+    po::launch_init_bf16(wqkv + (size_t)(qrows + kvrows) * h, kvrows, h, seed, layer_tid(l, K_V), 0, fan_scale(h),
                          po::INIT_PLAIN, s);
-    po::launch_init_bf16(ly.wo, h, ctxc, seed, layer_tid(l, K_O), 0, fan_scale(ctxc), po::INIT_PLAIN, s);
-    po::launch_init_bf16(ly.wgu, 2 * I, h, seed, layer_tid(l, K_GATE), layer_tid(l, K_UP), fan_scale(h),
+    if (f8) wrc |= quant(qkvc, h, ly.q_qkv, ly.s_qkv);
+    po::launch_init_bf16(f8 ? wtmp : ly.wo, h, ctxc, seed, layer_tid(l, K_O), 0, fan_scale(ctxc), po::INIT_PLAIN, s);
+    if (f8) wrc |= quant(h, ctxc, ly.q_o, ly.s_o);
+    po::launch_init_bf16(f8 ? wtmp : ly.wgu, 2 * I, h, seed, layer_tid(l, K_GATE), layer_tid(l, K_UP), fan_scale(h),
                          po::INIT_GATE_UP, s);
-    po::launch_init_bf16(ly.wdown, h, I, seed, layer_tid(l, K_DOWN), 0, fan_scale(I), po::INIT_PLAIN, s);
+    if (f8) wrc |= quant(2 * I, h, ly.q_gu, ly.s_gu);
+    po::launch_init_bf16(f8 ? wtmp : ly.wdown, h, I, seed, layer_tid(l, K_DOWN), 0, fan_scale(I), po::INIT_PLAIN, s);
+    if (f8) wrc |= quant(h, I, ly.q_down, ly.s_down);
     po::launch_init_norm(ly.attn_norm, h, seed, layer_tid(l, K_ATTN_NORM), s);
     if (c.qkv_bias) {
-      if (dalloc(e, &ly.bqkv, (size_t)qkvc * 4, &e->weight_bytes)) return fail(PO_ERR_CUDA, "bias allocation failed");
+      if (dalloc(e, &ly.bqkv, (size_t)qkvc * 4, &e->weight_bytes)) {
+        cudaFree(wtmp);
+        return fail(PO_ERR_CUDA, "bias allocation failed");
+      }
       po::launch_init_bias(ly.bqkv, qkvc, seed, layer_tid(l, K_QKV_BIAS), s);
     }
     po::launch_init_norm(ly.mlp_norm, h, seed, layer_tid(l, K_MLP_NORM), s);
-    if (po::make_tmap_b(&ly.map_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b(&ly.map_o, ly.wo, ctxc, h, ctxc) ||
-        po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I) ||
-        po::make_tmap_a(&ly.map2_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_a(&ly.map2_o, ly.wo, ctxc, h, ctxc) ||
-        po::make_tmap_a(&ly.map2_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_a(&ly.map2_down, ly.wdown, I, h, I) ||
-        po::make_tmap_b64(&ly.map3_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b64(&ly.map3_o, ly.wo, ctxc, h, ctxc) ||
-        po::make_tmap_b64(&ly.map3_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b64(&ly.map3_down, ly.wdown, I, h, I))
-      return fail(PO_ERR_CUDA, "weight tensor-map encode failed");
+    if (f8) {
+      if (po::make_tmap_a_f8(&ly.f8_qkv, ly.q_qkv, h, qkvc, h) || po::make_tmap_a_f8(&ly.f8_o, ly.q_o, ctxc, h, ctxc) ||
+          po::make_tmap_a_f8(&ly.f8_gu, ly.q_gu, h, 2 * I, h) || po::make_tmap_a_f8(&ly.f8_down, ly.q_down, I, h, I))
+        wrc = -2;
+    } else if (po::make_tmap_b(&ly.map_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_b(&ly.map_o, ly.wo, ctxc, h, ctxc) ||
+               po::make_tmap_b(&ly.map_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_b(&ly.map_down, ly.wdown, I, h, I) ||
+               po::make_tmap_a(&ly.map2_qkv, ly.wqkv, h, qkvc, h) || po::make_tmap_a(&ly.map2_o, ly.wo, ctxc, h, ctxc) ||
+               po::make_tmap_a(&ly.map2_gu, ly.wgu, h, 2 * I, h) || po::make_tmap_a(&ly.map2_down, ly.wdown, I, h, I) ||
+               po::make_tmap_b64(&ly.map3_qkv, ly.wqkv, h, qkvc, h) ||
+               po::make_tmap_b64(&ly.map3_o, ly.wo, ctxc, h, ctxc) ||
+               po::make_tmap_b64(&ly.map3_gu, ly.wgu, h, 2 * I, h) ||
+               po::make_tmap_b64(&ly.map3_down, ly.wdown, I, h, I)) {
+      wrc = -2;
+    }
   }
+  if (wtmp) {
+    cudaStreamSynchronize(s);
+    cudaFree(wtmp);
+  }
+  if (wrc) return fail(PO_ERR_CUDA, "weight quantisation / tensor-map encode failed");
 
   // ---- activation arena (hybrid prefill: full-length hidden/qkv, chunk-bounded MLP intermediate)
   const int xcols = h > ctxc ? h : ctxc;
@@ -261,6 +314,18 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       dalloc(e, &e->act, (size_t)chunk_rows * I * 2, &e->arena_bytes) ||
       dalloc(e, &e->rope, (size_t)T * (c.head_dim / 2) * sizeof(float2), &e->arena_bytes))
     return fail(PO_ERR_CUDA, "arena allocation failed");
+  if (f8 && (dalloc(e, &e->xg8, (size_t)T * h, &e->arena_bytes) ||
+             dalloc(e, &e->ctx8, (size_t)T * ctxc, &e->arena_bytes) ||
+             dalloc(e, &e->act8, (size_t)chunk_rows * I, &e->arena_bytes) ||
+             dalloc(e, &e->xg_s, (size_t)T * 4, &e->arena_bytes) ||
+             dalloc(e, &e->ctx_s, (size_t)T * 4, &e->arena_bytes) ||
+             dalloc(e, &e->act_s, (size_t)chunk_rows * 4, &e->arena_bytes)))
+    return fail(PO_ERR_CUDA, "FP8 arena allocation failed");
+  if (f8) {  // rows past a launch's M are read by its last tile: keep them finite (zero codes)
+    cudaMemsetAsync(e->xg8, 0, (size_t)T * h, s);
+    cudaMemsetAsync(e->ctx8, 0, (size_t)T * ctxc, s);
+    cudaMemsetAsync(e->act8, 0, (size_t)chunk_rows * I, s);
+  }
   cudaMemsetAsync(e->qkv, 0, (size_t)T * qkvc * 2, s);
   {
     // split-KV workspace: largest need over query lengths that trigger splitting, at n_total = max_tokens
@@ -272,11 +337,12 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       return fail(PO_ERR_CUDA, "attention workspace failed");
     // split-K workspace: largest need over the layer GEMM shapes for every M that triggers splitting
     size_t gw = 0;
+    auto ws_of = f8 ? po::gemm_split_ws_bytes_f8 : po::gemm_split_ws_bytes;
     for (int m = 1; m <= 148 * 128 && m <= T; m += 16) {
-      gw = std::max(gw, po::gemm_split_ws_bytes(m, qkvc, h));
-      gw = std::max(gw, po::gemm_split_ws_bytes(m, h, ctxc));
-      gw = std::max(gw, po::gemm_split_ws_bytes(m, 2 * I, h));
-      gw = std::max(gw, po::gemm_split_ws_bytes(m, h, I));
+      gw = std::max(gw, ws_of(m, qkvc, h));
+      gw = std::max(gw, ws_of(m, h, ctxc));
+      gw = std::max(gw, ws_of(m, 2 * I, h));
+      gw = std::max(gw, ws_of(m, h, I));
     }
     e->gemm_ws_bytes = gw;
     if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
@@ -314,6 +380,9 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       po::make_tmap_a(&e->map_xg, e->xg, h, T, h) ||
       po::make_tmap_a(&e->map_act, e->act, I, chunk_rows, I))
     return fail(PO_ERR_CUDA, "activation tensor-map encode failed");
+  if (f8 && (po::make_tmap_a_f8(&e->map_xg8, e->xg8, h, T, h) || po::make_tmap_a_f8(&e->map_ctx8, e->ctx8, ctxc, T, ctxc) ||
+             po::make_tmap_a_f8(&e->map_act8, e->act8, I, chunk_rows, I)))
+    return fail(PO_ERR_CUDA, "FP8 activation tensor-map encode failed");
 
   // ---- prefix pool: explicit size, or a profile run: what remains after weights + arena
   if (cudaStreamSynchronize(s) != cudaSuccess) return fail(PO_ERR_CUDA, "init kernels failed");
@@ -394,6 +463,48 @@ int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, 
   if (nelem != expect)
     return set_error(PO_ERR_ARG, "po_load_weight: kind %d expects %lld elements, got %lld", kind, (long long)expect,
                      (long long)nelem);
+  if (e->fp8() && (kind == 2 || kind == 3 || kind == 4 || kind == 5 || kind == 7 || kind == 8 || kind == 9)) {
+    // FP8 engine: the bf16 rows are quantised per row on the device into the E4M3 copy (+ scales)
+    int rows = 0, cols = h;
+    uint8_t* q = nullptr;
+    float* sc = nullptr;
+    switch (kind) {
+      case 2: rows = qrows; q = ly.q_qkv; sc = ly.s_qkv; break;
+      case 3: rows = kvrows; q = ly.q_qkv + (size_t)qrows * h; sc = ly.s_qkv + qrows; break;
+      case 4: rows = kvrows; q = ly.q_qkv + (size_t)(qrows + kvrows) * h; sc = ly.s_qkv + qrows + kvrows; break;
+      case 5: rows = h; cols = qrows; q = ly.q_o; sc = ly.s_o; break;
+      case 9: rows = h; cols = I; q = ly.q_down; sc = ly.s_down; break;
+      default: rows = I; break;  // 7 / 8: gate or up, interleaved below
+    }
+    __nv_bfloat16* tmp = nullptr;
+    uint8_t* tq = nullptr;
+    float* ts = nullptr;
+    int rc = 0;
+    if (cudaMalloc(&tmp, (size_t)rows * cols * 2) != cudaSuccess ||
+        cudaMalloc(&tq, (size_t)rows * cols) != cudaSuccess || cudaMalloc(&ts, (size_t)rows * 4) != cudaSuccess ||
+        cudaMemcpy(tmp, host, (size_t)rows * cols * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
+        po::quantize_rows_e4m3(tmp, cols, rows, cols, tq, cols, ts, nullptr) != 0 ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      rc = -1;
+    if (!rc && (kind == 7 || kind == 8)) {
+      // interleave 16-row groups into the fused gate/up layout, gate first (rows and their scales)
+      const int off = kind == 7 ? 0 : 16;
+      for (int g = 0; g < I / 16 && !rc; ++g)
+        if (cudaMemcpy(ly.q_gu + ((size_t)g * 32 + off) * h, tq + (size_t)g * 16 * h, (size_t)16 * h,
+                       cudaMemcpyDeviceToDevice) != cudaSuccess ||
+            cudaMemcpy(ly.s_gu + (size_t)g * 32 + off, ts + (size_t)g * 16, 16 * 4, cudaMemcpyDeviceToDevice) !=
+                cudaSuccess)
+          rc = -1;
+    } else if (!rc) {
+      if (cudaMemcpy(q, tq, (size_t)rows * cols, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+          cudaMemcpy(sc, ts, (size_t)rows * 4, cudaMemcpyDeviceToDevice) != cudaSuccess)
+        rc = -1;
+    }
+    cudaFree(tmp);
+    cudaFree(tq);
+    cudaFree(ts);
+    return rc ? set_error(PO_ERR_CUDA, "po_load_weight: FP8 quantisation / copy failed") : PO_OK;
+  }
   if (kind == 7 || kind == 8) {
     // interleave into the fused gate/up layout: 16-row groups, gate first
     const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(host);
@@ -463,6 +574,18 @@ int gemm(const CUtensorMap& a, const void* x, long long ldx, const CUtensorMap& 
   return po::gemm_use_pair(g.M) ? po::gemm_launch_pair(*am, b2, epi, g, s, &b3) : po::gemm_launch(*am, b1, epi, g, s);
 }
 
+// weight_fp8: quantise the launch's A rows [a_row0, a_row0 + M) per row (E4M3 + scale), then the W8A8 pair GEMM
+// with the weight's per-channel scales. Two launches.
+int gemm8(const CUtensorMap& a8, const __nv_bfloat16* x, long long ldx, uint8_t* x8, float* xs, const CUtensorMap& b8,
+          const float* bs, int epi, po::GemmArgs g, cudaStream_t s) {
+  if (int rc = po::quantize_rows_e4m3(x + (size_t)g.a_row0 * ldx, ldx, g.M, g.K, x8 + (size_t)g.a_row0 * g.K, g.K,
+                                      xs + g.a_row0, s))
+    return rc;
+  g.a_scale = xs + g.a_row0;
+  g.b_scale = bs;
+  return po::gemm_launch_pair_f8(a8, b8, epi, g, s);
+}
+
 // PO_BOUNDED_A=0 keeps the whole-buffer activation maps (A/B runs)
 bool bounded_a_enabled() {
   static int on = -1;
@@ -496,6 +619,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
   const int h = c.hidden, I = c.intermediate, L = c.num_layers;
   const int qkvc = e->qkv_cols(), ctxc = e->ctx_cols(), kvd = e->kv_dim();
   const int kv_col0 = c.n_heads * c.head_dim;
+  const bool f8 = e->fp8();
   int launches = 0;
   auto mark = [&](int cls, bool begin) {
     if (!e->profiling) return;
@@ -555,9 +679,12 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     }
     norm_in(g, e->ss_attn);
     mark(KC_QKV, true);
-    rc |= gemm(e->map_xg, e->xg, h, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
+    if (f8)
+      rc |= gemm8(e->map_xg8, e->xg, h, e->xg8, e->xg_s, ly.f8_qkv, ly.s_qkv, po::EPI_QKV_ROPE, g, s);
+    else
+      rc |= gemm(e->map_xg, e->xg, h, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
     mark(KC_QKV, false);
-    ++launches;
+    launches += f8 ? 2 : 1;
     // the last layer only needs the final row's output (the LM head reads nothing else); its K/V rows
     // were computed (and admitted to the pool) above
     const bool last_only = c.last_row_only && l == L - 1 && n_miss > 1;
@@ -576,9 +703,12 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     mark(KC_O, true);
-    rc |= gemm(e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go, s);
+    if (f8)
+      rc |= gemm8(e->map_ctx8, e->xn, ctxc, e->ctx8, e->ctx_s, ly.f8_o, ly.s_o, po::EPI_RESID_F32, go, s);
+    else
+      rc |= gemm(e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go, s);
     mark(KC_O, false);
-    ++launches;
+    launches += f8 ? 2 : 1;
     for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
       const int cr = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
       po::GemmArgs gu{};
@@ -586,16 +716,22 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
       norm_in(gu, e->ss_mlp + (size_t)lo * nseg);
       mark(KC_GATE_UP, true);
-      rc |= gemm(e->map_xg, e->xg, h, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu, s);
+      if (f8)
+        rc |= gemm8(e->map_xg8, e->xg, h, e->xg8, e->xg_s, ly.f8_gu, ly.s_gu, po::EPI_SILU_MUL, gu, s);
+      else
+        rc |= gemm(e->map_xg, e->xg, h, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu, s);
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
       norm_out(gd, e->xg + (size_t)lo * h, gamma_next_layer, e->ss_attn + (size_t)lo * nseg);
       mark(KC_DOWN, true);
-      rc |= gemm(e->map_act, e->act, I, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd, s);
+      if (f8)
+        rc |= gemm8(e->map_act8, e->act, I, e->act8, e->act_s, ly.f8_down, ly.s_down, po::EPI_RESID_F32, gd, s);
+      else
+        rc |= gemm(e->map_act, e->act, I, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd, s);
       mark(KC_DOWN, false);
-      launches += 2;
+      launches += f8 ? 4 : 2;
     }
   }
   if (rc) return set_error(PO_ERR_CUDA, "po_prefill: kernel launch failed (%d): %s", rc,

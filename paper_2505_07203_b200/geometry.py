@@ -47,6 +47,8 @@ def arena_bytes(m: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK) -> 
     rows = min(chunk, T)
     b = 4 * T * h + 2 * T * max(h, ctx) + 2 * T * qkvc + 2 * rows * m.intermediate + 8 * T * (hd // 2)
     b += 2 * T * h + 2 * 4 * T * (h // 128)  # folded-RMSNorm input xg (bf16) + two sum-of-squares buffers
+    if m.weight_fp8:  # E4M3 copies of the GEMM inputs (xg, ctx, act) + their per-row scales
+        b += T * h + T * ctx + rows * m.intermediate + 4 * (2 * T + rows)
     max_blocks = T // 16 + 1
     b += 4 * T + 4 * max_blocks + 4 * max_blocks + 3 * 4 * m.vocab + 16
     return b

@@ -151,3 +151,67 @@ def test_gemm_fp8_rejects_bad_shape_and_missing_scales():
     with pytest.raises(_lib.PrefillOnlyError):  # K % 128
         _lib.call("po_op_gemm_fp8", _p(Aq), 128, _p(sa), _p(Bq), 128, _p(sb), _p(out), 256, None, 0, 64, 256, 64,
                   _lib.EPI_BF16, None, 0, 0, None)
+
+
+# ---- the FP8 engine (W8A8 layer GEMMs) against the oracle's FP8 emulation (oracle/llama_ref.py quantize_rows)
+import numpy as np  # noqa: E402
+
+from oracle import llama_ref  # noqa: E402
+from paper_2505_07203_b200.config import ModelConfig, TINY_FP8  # noqa: E402
+from paper_2505_07203_b200.engine import Engine  # noqa: E402
+
+LOGIT_ATOL = 2e-2
+LOGIT_RTOL = 2e-2
+YES_NO = [9642, 2822]
+TINY_QWEN_FP8 = ModelConfig("tiny-qwen-fp8", 2, 1280, 10, 2, 128, 1024, 32000, rms_eps=1e-6, rope_theta=1_000_000.0,
+                            rope_scaling=0, qkv_bias=True, weight_fp8=True)
+
+
+def tokens_for(seed, n):
+    return np.random.default_rng([seed, 0, 0]).integers(0, 2 ** 32, size=n, dtype=np.uint32)
+
+
+def check_fp8(model, res, toks, allowed, seed, n_cached=0):
+    cfg = llama_ref.Cfg.from_model(model)
+    assert cfg.weight_fp8
+    logits, probs, am = llama_ref.llama_forward(cfg, llama_ref.make_weights(cfg, seed), toks, allowed)
+    err = np.abs(res.logits - logits)
+    tol = LOGIT_ATOL + LOGIT_RTOL * np.abs(logits)
+    print(f"{model.name}: n={len(toks)} n_c={n_cached} gpu={res.logits} oracle={logits} max_err={err.max():.3e}")
+    assert (err <= tol).all(), (res.logits, logits)
+    srt = np.sort(logits)[::-1]
+    if len(srt) > 1 and srt[0] - srt[1] > 2 * tol.max():
+        assert res.index == am
+    assert abs(float(res.probs.sum()) - 1.0) < 1e-5
+
+
+def test_tiny_fp8_engine_matches_oracle_cold_ragged_and_hit():
+    with Engine(TINY_FP8, seed=42, max_tokens=4096, chunk=1024, pool_blocks=256) as e:
+        toks = tokens_for(0, 2048)
+        slots = list(range(128))
+        check_fp8(TINY_FP8, e.prefill(toks, YES_NO, 0, slots), toks, YES_NO, 42)
+        check_fp8(TINY_FP8, e.prefill(toks, YES_NO, 1024, slots), toks, YES_NO, 42, 1024)  # prefix hit (split-K)
+        for n in (1, 130):
+            t = tokens_for(n, n)
+            check_fp8(TINY_FP8, e.prefill(t, YES_NO), t, YES_NO, 42)
+
+
+def test_qwen_style_fp8_odd_group_and_bias():
+    toks = tokens_for(17, 1300)
+    with Engine(TINY_QWEN_FP8, seed=5, max_tokens=2048, chunk=512, pool_blocks=128) as e:
+        check_fp8(TINY_QWEN_FP8, e.prefill(toks, YES_NO), toks, YES_NO, 5)
+
+
+def test_fp8_engine_load_weight_roundtrip():
+    """po_load_weight on an FP8 engine quantises the given bf16 rows: loading the engine's own init reproduces it."""
+    toks = tokens_for(3, 700)
+    cfg = llama_ref.Cfg.from_model(TINY_FP8)
+    w = llama_ref.make_weights(llama_ref.Cfg(**{**cfg.__dict__, "weight_fp8": False}), 42)  # bf16 init
+    with Engine(TINY_FP8, seed=42, max_tokens=1024, chunk=512, pool_blocks=8) as e:
+        before = e.prefill(toks, YES_NO).logits
+        for l, lw in enumerate(w["layers"]):
+            for kind, name in ((2, "wq"), (3, "wk"), (4, "wv"), (5, "wo"), (7, "w_gate"), (8, "w_up"), (9, "w_down")):
+                bits = (np.ascontiguousarray(lw[name], dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+                e.load_weight(kind, l, bits)  # bf16 bit patterns (the oracle's values are exact bf16)
+        after = e.prefill(toks, YES_NO).logits
+    assert np.array_equal(before, after)
