@@ -1,6 +1,6 @@
 """Measurements for the BASELINE configs beyond the headline (configs[0], [2], [4]); writes one JSON per config.
 
-  python tools/bench_configs.py tiny|llama128k|qwen32b [out.json]
+  python tools/bench_configs.py tiny|llama128k|qwen32b|jct|fp8 [out.json]
 
 tiny       2-layer d=256 model, one 2,048-token Yes/No request: GPU latency, oracle CPU latency, parity.
 llama128k  Llama-3.1-8B, one 131,072-token request on one GPU (hybrid prefill + one-layer KV): latency,
@@ -8,6 +8,8 @@ llama128k  Llama-3.1-8B, one 131,072-token request on one GPU (hybrid prefill + 
 qwen32b    Qwen-2.5-32B bf16 random-init, credit-verification documents U[10k, 60k] (60 users x 1 request):
            service time per length, tokens/s, and QPS at the P99 SLO over 8 replicas (virtual-clock loop,
            every distinct shape run for real on this GPU).
+fp8        the FP8-weight presets (W8A8 E4M3 layer GEMMs): Qwen-2.5-32B-FP8 at 10k/35k/60k, Llama-3.3-70B-FP8 at
+           20k, and Llama-3.1-8B with FP8 weights at 20k next to its bf16 headline; cold and prefix-hit service.
 """
 
 import json
@@ -127,9 +129,37 @@ def jct():
             "grid": [[s.n_input, s.n_cached, s.latency] for s in samples]}
 
 
+def fp8():
+    from paper_2505_07203_b200.config import LLAMA_3_3_70B_FP8, QWEN_2_5_32B_FP8, replace
+
+    out = {"config": "FP8-weight presets (ps/presets/qwen-32b-fp8.preset, llama-3.3-70b-fp8.preset): E4M3 layer "
+                     "weights with per-channel scales, per-row dynamic E4M3 activations, tcgen05 kind::f8f6f4",
+           "models": {}}
+    cases = [(QWEN_2_5_32B_FP8, (10_000, 35_000, 60_000)), (LLAMA_3_3_70B_FP8, (20_000,)),
+             (replace(LLAMA_3_1_8B, name="llama-3.1-8b-fp8", weight_fp8=True), (20_000,))]
+    for M, lengths in cases:
+        n_max = max(lengths)
+        with Engine(M, seed=0, max_tokens=n_max, pool_blocks=n_max // 16 + 8) as e:
+            e.prefill(toks(2, 4096), YES_NO)
+            rows = {}
+            for n in lengths:
+                t = toks(3, n)
+                slots = list(range(n // 16))
+                e.prefill(t, YES_NO, 0, slots)  # warm + admit
+                cold = min(e.prefill(t, YES_NO).service_s for _ in range(3))
+                nc = (n - 160) // 16 * 16
+                hit = statistics.median(e.prefill(t, YES_NO, nc, slots).service_s for _ in range(10))
+                rows[n] = {"cold_s": cold, "tokens_per_s": n / cold,
+                           "algorithmic_tflops": M.request_flops(n) / cold / 1e12,
+                           "executed_tflops": executed_flops(M, n) / cold / 1e12,
+                           "hit_s": hit, "hit_n_cached": nc}
+            out["models"][M.name] = {"weight_gb": e.weight_bytes / 1e9, "pool_blocks": e.pool_blocks, "per_length": rows}
+    return out
+
+
 if __name__ == "__main__":
     which = sys.argv[1]
-    out = {"tiny": tiny, "llama128k": llama128k, "qwen32b": qwen32b, "jct": jct}[which]()
+    out = {"tiny": tiny, "llama128k": llama128k, "qwen32b": qwen32b, "jct": jct, "fp8": fp8}[which]()
     text = json.dumps(out)
     print(text, flush=True)
     if len(sys.argv) > 2:
