@@ -168,6 +168,13 @@ def run_reference(args, world, rank):
     """--impl reference: the reference path's CPU implementation (the oracle port) on the host cores."""
     if rank != 0:
         return
+    # every host thread for the BLAS (torchrun sets OMP_NUM_THREADS=1 for its workers; the other ranks idle here)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        limits = threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
+    except Exception:
+        limits = None
     run, flops = cpu_layer_sample()
     for _ in range(args.warmup):
         run()
@@ -179,6 +186,8 @@ def run_reference(args, world, rank):
     t = sum(times)
     value = cpu_tokens_per_s(t / args.steps, flops, args.n_tokens)
     cores = blas_threads()
+    if limits is not None:
+        limits.restore_original_limits()
     sample = (f"one Llama-3.1-8B layer (RMSNorm, QKV+RoPE, causal GQA attention, O, SiLU MLP) at 1,024 tokens in "
               f"float64 numpy per step, extrapolated by the FLOP formula to 32 layers x {args.n_tokens} tokens")
     print(json.dumps({
