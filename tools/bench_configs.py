@@ -1,6 +1,6 @@
 """Measurements for the BASELINE configs beyond the headline (configs[0], [2], [4]); writes one JSON per config.
 
-  python tools/bench_configs.py tiny|llama128k|qwen32b|jct|fp8 [out.json]
+  python tools/bench_configs.py tiny|llama128k|qwen32b|qwen32b_fp8|jct|fp8 [out.json]
 
 tiny       2-layer d=256 model, one 2,048-token Yes/No request: GPU latency, oracle CPU latency, parity.
 llama128k  Llama-3.1-8B, one 131,072-token request on one GPU (hybrid prefill + one-layer KV): latency,
@@ -78,11 +78,11 @@ def llama128k():
                     "the rest of HBM is the prefix pool (profile run)"}
 
 
-def qwen32b(slo=30.0):
+def qwen32b(slo=30.0, model=None):
     from paper_2505_07203_b200.scheduling import Policy
     from paper_2505_07203_b200.serving import MeasuredServiceFn, qps_at_slo, simulate, sweep_rates
 
-    M = QWEN_2_5_32B
+    M = model or QWEN_2_5_32B
     trace = wl.gen_credit_verification(0, wl.CREDIT_10K_60K)
     with Engine(M, seed=0, max_tokens=60_000, pool_blocks=4096) as e:
         t = toks(2, 10_000)
@@ -101,8 +101,9 @@ def qwen32b(slo=30.0):
         res = sweep_rates(trace, rates, seed=0, run=run, keep_sessions=False)
     best = qps_at_slo(res, slo)
     rep = dict(res)[best] if best else None
-    return {"config": "Qwen-2.5-32B bf16 random-init (64 L, 5120, 40/8 heads, q/k/v bias), credit-verification "
-                      "documents U[10k, 60k], 60 users x 1 request, 8 replicas (BASELINE configs[4])",
+    return {"config": f"{M.name} ({'E4M3 W8A8' if M.weight_fp8 else 'bf16'}) random-init (64 L, 5120, 40/8 heads, "
+                      "q/k/v bias), credit-verification documents U[10k, 60k], 60 users x 1 request, 8 replicas "
+                      "(BASELINE configs[4])",
             "per_length": per_len, "qps_at_slo": best, "slo_p99_s": slo, "saturation_rps": sat,
             "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
             "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency} for q, r in res],
@@ -159,7 +160,9 @@ def fp8():
 
 if __name__ == "__main__":
     which = sys.argv[1]
-    out = {"tiny": tiny, "llama128k": llama128k, "qwen32b": qwen32b, "jct": jct, "fp8": fp8}[which]()
+    from paper_2505_07203_b200.config import QWEN_2_5_32B_FP8
+    out = {"tiny": tiny, "llama128k": llama128k, "qwen32b": qwen32b, "jct": jct, "fp8": fp8,
+           "qwen32b_fp8": lambda: qwen32b(model=QWEN_2_5_32B_FP8)}[which]()
     text = json.dumps(out)
     print(text, flush=True)
     if len(sys.argv) > 2:
