@@ -33,5 +33,24 @@ for model in (TINY, SMALL):
         e.prefill(t[:600], [1, 2], 0, slots[:37])
         e.prefill(t[:600], [1, 2], 512, slots[:37])
         e.prefill(t, [1, 2], 592, slots)  # straddling tile + suffix admission
+# FP8: per-row quantisation, the W8A8 pair GEMM (full tiles, ragged M, split-K) with every epilogue, and an FP8 engine
+from paper_2505_07203_b200.config import TINY_FP8
+for M, N, K in ((300, 512, 256), (160, 512, 2048), (1, 256, 1024)):
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    Aq = torch.empty(M, K, dtype=torch.uint8, device="cuda"); sa = torch.empty(M, device="cuda")
+    Bq = torch.empty(N, K, dtype=torch.uint8, device="cuda"); sb = torch.empty(N, device="cuda")
+    _lib.call("po_op_quantize_e4m3", p(A), K, M, K, p(Aq), K, p(sa), None)
+    _lib.call("po_op_quantize_e4m3", p(B), K, N, K, p(Bq), K, p(sb), None)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    resid = torch.zeros(M, N, device="cuda")
+    for epi in (0, 1, 2):
+        _lib.call("po_op_gemm_fp8", p(Aq), K, p(sa), p(Bq), K, p(sb), p(out), N, p(resid), N, M, N, K, epi, None, 0, 0,
+                  None)
+with Engine(TINY_FP8, seed=1, max_tokens=1024, chunk=256, pool_blocks=64) as e:
+    t = np.random.default_rng(1).integers(0, 2**32, size=700, dtype=np.uint32)
+    slots = list(range(700 // 16))
+    e.prefill(t, [1, 2], 0, slots)
+    e.prefill(t, [1, 2], 512, slots)
 torch.cuda.synchronize()
 print("sanitize workload done")
