@@ -465,7 +465,7 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
     """
     from paper_2505_07203_b200 import workload as wl
     from paper_2505_07203_b200.scheduling import Policy
-    from paper_2505_07203_b200.serving import ReplayServiceFn, qps_at_slo as pick, simulate, sweep_rates
+    from paper_2505_07203_b200.serving import ReplayServiceFn, qps_at_slo as pick, refine_qps, simulate, sweep_rates
 
     if rank != 0:
         return None
@@ -479,6 +479,9 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
     rates = [sat * m for m in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0)]
     res = sweep_rates(trace, rates, seed=0, run=run)
     fifo = sweep_rates(trace, rates, seed=0, run=lambda tr: run(tr, Policy.fifo()))
+    # resolve the knee: bisect between the last rate meeting the SLO and the first one above it that misses
+    res = refine_qps(res, slo, lambda q: sweep_rates(trace, [q], seed=0, run=run)[0][1])
+    fifo = refine_qps(fifo, slo, lambda q: sweep_rates(trace, [q], seed=0, run=lambda tr: run(tr, Policy.fifo()))[0][1])
     best = pick(res, slo)
     rep = dict(res)[best] if best else None
     hits = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc > 0)
@@ -489,8 +492,11 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         "miss_tokens_per_s_at_slo": rep.miss_tokens_per_s if rep else None,
         "p99_at_value_s": rep.p99_latency if rep else None,
         "fifo_qps_at_slo": pick(fifo, slo), "saturation_rps": sat,
-        "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency, "hit_requests": r.cache_hit_requests,
-                   "fifo_p99_s": f.p99_latency} for (q, r), (_, f) in zip(res, fifo)],
+        "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency, "hit_requests": r.cache_hit_requests}
+                  for q, r in res],
+        "fifo_sweep": [{"rate": q, "p99_s": f.p99_latency} for q, f in fifo],
+        "search": "grid of 0.25-2.0 x the saturation rate, then 5 bisection steps between the last rate meeting the "
+                  "SLO and the next one missing it",
         "workload": "post-recommendation 40 users x 50 requests, profiles 19,850 +- 3,000 tokens + 150-token "
                     "suffix, Poisson arrivals (user sessions contiguous), Yes/No allowed ids",
         "method": f"virtual-clock serving loop with the reference's event semantics (calibrated SRJF, prefix pool of "

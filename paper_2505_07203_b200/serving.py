@@ -316,6 +316,30 @@ def qps_at_slo(results, slo_s: float) -> float:
     return max(ok) if ok else 0.0
 
 
+def refine_qps(results, slo_s: float, evaluate: Callable, steps: int = 5):
+    """Bisect between the largest swept rate that meets the SLO and the next swept rate above it that misses, so
+    QPS@SLO is resolved to (gap / 2^steps) instead of the sweep's grid. evaluate(rate) -> ServeReport. Returns the
+    results with the bisection points added, sorted by rate."""
+    res = sorted(results, key=lambda x: x[0])
+    ok = [q for q, rep in res if rep.p99_latency <= slo_s]
+    if not ok:
+        return res
+    lo = max(ok)
+    above = [q for q, rep in res if q > lo and rep.p99_latency > slo_s]
+    if not above:
+        return res
+    hi = min(above)
+    for _ in range(steps):
+        mid = 0.5 * (lo + hi)
+        rep = evaluate(mid)
+        res.append((mid, rep))
+        if rep.p99_latency <= slo_s:
+            lo = mid
+        else:
+            hi = mid
+    return sorted(res, key=lambda x: x[0])
+
+
 # ------------------------------------------------------------------ wall-clock server
 
 

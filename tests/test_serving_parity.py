@@ -115,3 +115,24 @@ def test_replay_service_fn_records_each_request_once_and_reuses():
     rep1 = simulate(wl.zero_arrivals(trace), 1, Policy.srjf_calibrated(), 400_000, svc)
     assert eng.calls == calls  # same order and cache state: all reused
     assert rep1.p99_latency == rep0.p99_latency
+
+
+def test_refine_qps_bisects_to_the_knee():
+    from types import SimpleNamespace
+
+    from paper_2505_07203_b200.serving import qps_at_slo, refine_qps
+
+    knee = 7.3
+    rep = lambda q: SimpleNamespace(p99_latency=1.0 if q <= knee else 10.0)  # noqa: E731
+    grid = [(q, rep(q)) for q in (2.0, 4.0, 6.0, 8.0, 10.0)]
+    assert qps_at_slo(grid, 2.0) == 6.0
+    calls = []
+    out = refine_qps(grid, 2.0, lambda q: calls.append(q) or rep(q), steps=6)
+    assert len(calls) == 6 and all(6.0 < q < 8.0 for q in calls)
+    best = qps_at_slo(out, 2.0)
+    assert knee - 2.0 / 2 ** 6 <= best <= knee
+    assert [q for q, _ in out] == sorted(q for q, _ in out)
+    # nothing to refine: every rate passes, or none does
+    never = lambda q: 1 / 0  # noqa: E731  (must not be called)
+    assert [q for q, _ in refine_qps([(1.0, rep(1.0))], 2.0, never)] == [1.0]
+    assert [q for q, _ in refine_qps([(9.0, rep(9.0))], 2.0, never)] == [9.0]
