@@ -482,6 +482,12 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
     # resolve the knee: bisect between the last rate meeting the SLO and the first one above it that misses
     res = refine_qps(res, slo, lambda q: sweep_rates(trace, [q], seed=0, run=run)[0][1])
     fifo = refine_qps(fifo, slo, lambda q: sweep_rates(trace, [q], seed=0, run=lambda tr: run(tr, Policy.fifo()))[0][1])
+    # the paper's default fairness weight (lambda = 500) beside the reference's (0.5, same units: miss
+    # tokens per second of queueing)
+    pol500 = Policy.srjf_calibrated(lam=500.0)
+    run500 = lambda tr: run(tr, pol500)  # noqa: E731
+    res500 = refine_qps(sweep_rates(trace, rates, seed=0, run=run500), slo,
+                        lambda q: sweep_rates(trace, [q], seed=0, run=run500)[0][1])
     best = pick(res, slo)
     rep = dict(res)[best] if best else None
     hits = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc > 0)
@@ -491,7 +497,7 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
         "miss_tokens_per_s_at_slo": rep.miss_tokens_per_s if rep else None,
         "p99_at_value_s": rep.p99_latency if rep else None,
-        "fifo_qps_at_slo": pick(fifo, slo), "saturation_rps": sat,
+        "fifo_qps_at_slo": pick(fifo, slo), "lambda500_qps_at_slo": pick(res500, slo), "saturation_rps": sat,
         "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency, "hit_requests": r.cache_hit_requests}
                   for q, r in res],
         "fifo_sweep": [{"rate": q, "p99_s": f.p99_latency} for q, f in fifo],
