@@ -471,8 +471,14 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         return None
     trace = wl.gen_post_recommendation(0, wl.POSTREC_20K)
     capacity = min(eng.capacity_tokens, 16 * eng.pool_blocks)
-    svc = ReplayServiceFn(eng, ALLOWED)
     t0 = time.perf_counter()
+    # the paper's calibration: JCT profile fitted on this GPU's measured latencies
+    # (ps/jct.py:100-128 with the real engine as latency_fn), seconds-valued scores, lambda = 500
+    from paper_2505_07203_b200 import jct as J
+    from paper_2505_07203_b200.scheduling import SCORING_PROFILE
+
+    jprof = J.fit(J.profile_engine(eng, max_input=24_000, step=4000))
+    svc = ReplayServiceFn(eng, ALLOWED)
     run = lambda tr, pol=None: simulate(tr, world, pol or Policy.srjf_calibrated(), capacity, svc)  # noqa: E731
     sat = run(wl.zero_arrivals(trace)).throughput  # every request runs for real here, in serving order
     svc.recording = False
@@ -488,6 +494,10 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
     run500 = lambda tr: run(tr, pol500)  # noqa: E731
     res500 = refine_qps(sweep_rates(trace, rates, seed=0, run=run500), slo,
                         lambda q: sweep_rates(trace, [q], seed=0, run=run500)[0][1])
+    polp = Policy.srjf_calibrated(lam=500.0, scoring=SCORING_PROFILE)
+    runp = lambda tr: simulate(tr, world, polp, capacity, svc, jct_profile=jprof)  # noqa: E731
+    resp = refine_qps(sweep_rates(trace, rates, seed=0, run=runp), slo,
+                      lambda q: sweep_rates(trace, [q], seed=0, run=runp)[0][1])
     best = pick(res, slo)
     rep = dict(res)[best] if best else None
     hits = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc > 0)
@@ -497,7 +507,11 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
         "miss_tokens_per_s_at_slo": rep.miss_tokens_per_s if rep else None,
         "p99_at_value_s": rep.p99_latency if rep else None,
-        "fifo_qps_at_slo": pick(fifo, slo), "lambda500_qps_at_slo": pick(res500, slo), "saturation_rps": sat,
+        "fifo_qps_at_slo": pick(fifo, slo), "lambda500_qps_at_slo": pick(res500, slo),
+        "profile_lambda500_qps_at_slo": pick(resp, slo),
+        "jct_profile": {"coef_input": jprof.coef_input, "coef_cached": jprof.coef_cached,
+                        "intercept": jprof.intercept, "fit_r2": jprof.fit_r2},
+        "saturation_rps": sat,
         "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency, "hit_requests": r.cache_hit_requests}
                   for q, r in res],
         "fifo_sweep": [{"rate": q, "p99_s": f.p99_latency} for q, f in fifo],
