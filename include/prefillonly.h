@@ -26,7 +26,7 @@ extern "C" {
 #define PO_ERR_CAPACITY (-3) /* CapacityError: request beyond MIL             (ps/costs.py:40-45,270-274)        */
 #define PO_ERR_CUDA (-4)     /* CUDA runtime / launch failure                                                    */
 #define PO_ERR_ARG (-5)      /* invalid argument (null pointer, bad shape)                                       */
-#define PO_ERR_POOL (-6)     /* prefix-pool slot out of range                                                    */
+#define PO_ERR_POOL (-6)     /* prefix-pool slot out of range, or one slot named twice in a request              */
 
 const char* po_last_error(void);
 const char* po_version(void);

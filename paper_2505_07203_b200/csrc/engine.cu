@@ -92,6 +92,8 @@ struct po_engine {
   int64_t pool_blocks = 0;
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
+  std::vector<uint32_t> slot_stamp;  // per pool slot: the last request that named it (collision check)
+  uint32_t stamp_gen = 0;
   float last_ms = 0.f;
   float last_enqueue_ms = 0.f;  // host time to enqueue the forward (launch-bound when it approaches last_ms)
   int last_launches = 0;
@@ -541,6 +543,13 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
   const int cached_blocks = (n_c + bt - 1) / bt;
   int n_admit = 0;
   for (int b = 0; b <= n / bt; ++b) e->h_kvslot[b] = -1;
+  // a slot may appear once per request: two admitted blocks on one slot race in the QKV epilogue, and an admitted
+  // block on a cached block's slot would overwrite keys this forward's attention still reads
+  if ((int64_t)e->slot_stamp.size() != e->pool_blocks) e->slot_stamp.assign((size_t)e->pool_blocks, 0u);
+  if (++e->stamp_gen == 0) {
+    std::fill(e->slot_stamp.begin(), e->slot_stamp.end(), 0u);
+    e->stamp_gen = 1;
+  }
   for (int b = 0; b < n_blocks; ++b) {
     const int slot = pool_block_ids[b];
     if (b < n_cached / bt) {
@@ -551,7 +560,12 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
       if (slot >= e->pool_blocks) return set_error(PO_ERR_POOL, "po_prefill: admit slot %d out of range", slot);
       e->h_kvslot[b] = slot;
       ++n_admit;
+    } else {
+      continue;
     }
+    if (e->slot_stamp[slot] == e->stamp_gen)
+      return set_error(PO_ERR_POOL, "po_prefill: pool slot %d named twice in one request (block %d)", slot, b);
+    e->slot_stamp[slot] = e->stamp_gen;
   }
   *n_admit_out = n_admit;
   return n_c;

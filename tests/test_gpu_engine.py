@@ -202,3 +202,29 @@ def test_short_suffix_admission_feeds_later_hits(model):
         c = eng.prefill(c_toks, allowed, n_cached=800, pool_block_ids=slots[:50] + [-1] * 3)
         assert c.n_cached == 800
         check_against_oracle(model, c, c_toks, allowed, 42)
+
+
+def test_request_validation_errors(tiny_engine):
+    """Bad requests fail loudly with the reference taxonomy and leave the engine usable."""
+    from paper_2505_07203_b200._lib import PrefillOnlyError
+
+    toks = tokens_for(30, 256)
+    slots = list(range(300, 316))
+    bad = [
+        dict(tokens=toks[:0], allowed=YES_NO),                                    # empty request
+        dict(tokens=toks, allowed=[]),                                           # empty allowed list
+        dict(tokens=toks, allowed=[32_000]),                                     # id past the vocab
+        dict(tokens=toks, allowed=[-1]),
+        dict(tokens=toks, allowed=YES_NO, n_cached=8, pool_block_ids=slots),     # not block aligned
+        dict(tokens=toks, allowed=YES_NO, n_cached=272, pool_block_ids=slots),   # n_cached > n
+        dict(tokens=toks, allowed=YES_NO, n_cached=32, pool_block_ids=[1]),      # cached blocks without slots
+        dict(tokens=toks, allowed=YES_NO, n_cached=0, pool_block_ids=[10 ** 6]),  # admit slot out of range
+        dict(tokens=toks, allowed=YES_NO, n_cached=0, pool_block_ids=[7, 7]),    # two admitted blocks, one slot
+        dict(tokens=toks, allowed=YES_NO, n_cached=16, pool_block_ids=[7, 7]),   # admission over a cached block
+    ]
+    for kw in bad:
+        with pytest.raises((PrefillOnlyError, ValueError)):
+            tiny_engine.prefill(**kw)
+    ok = tiny_engine.prefill(toks, [5, 5, 9])  # duplicate allowed ids are legal: equal logits, first max wins
+    assert ok.logits[0] == ok.logits[1] and ok.index != 1
+    check_against_oracle(TINY, tiny_engine.prefill(toks, YES_NO), toks, YES_NO, 42)
