@@ -92,6 +92,7 @@ struct po_engine {
   int64_t pool_blocks = 0;
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
+  bool act_persist = false;  // the MLP chunk buffer is pinned in L2 (persisting access-policy window)
   std::vector<uint32_t> slot_stamp;  // per pool slot: the last request that named it (collision check)
   uint32_t stamp_gen = 0;
   float last_ms = 0.f;
@@ -175,6 +176,10 @@ int po_free(po_engine* e) {
   if (!e) return PO_OK;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->act_persist) {  // hand the persisting L2 carve-out back
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
   for (void* p : e->allocs) cudaFree(p);
   cudaFreeHost(e->h_tokens);
   cudaFreeHost(e->h_slots);
@@ -377,6 +382,31 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
         cudaSuccess)
       return fail(PO_ERR_CUDA, "rope table upload failed");
     cudaStreamSynchronize(s);
+  }
+  {
+    // L2-resident MLP intermediate: when the chunk buffer (gate/up output = down input) fits the persisting L2
+    // carve-out (chunk <= ~2800 rows for Llama-8B), pin it with a persisting access-policy window so it never
+    // streams to HBM; the weight streams otherwise evict it (ncu: profiles/r1_mlp_l2_summary.md).
+    // PO_ACT_PERSIST=0 disables, =1 forces a (partial) window.
+    const char* v = getenv("PO_ACT_PERSIST");
+    const size_t act_bytes = (size_t)chunk_rows * I * 2;
+    int dev = 0, max_persist = 0, max_window = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    const bool on = v ? v[0] == '1' : (max_persist > 0 && act_bytes <= (size_t)max_persist);
+    if (on && max_window > 0) {
+      const size_t win = std::min(act_bytes, (size_t)max_window);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(win, (size_t)max_persist));
+      cudaStreamAttrValue at = {};
+      at.accessPolicyWindow.base_ptr = e->act;
+      at.accessPolicyWindow.num_bytes = win;
+      at.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
+      at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &at);
+      e->act_persist = true;
+    }
   }
   if (po::make_tmap_a(&e->map_xn, e->xn, h, T, h) || po::make_tmap_a(&e->map_ctx, e->xn, ctxc, T, ctxc) ||
       po::make_tmap_a(&e->map_xg, e->xg, h, T, h) ||
