@@ -116,7 +116,8 @@ int po_free(po_engine* e);
  * (b < n_cached/block_tokens) the slot holding block b; for later blocks the slot to admit block b into, or
  * -1 (suffix discard, ps/cache.py:143-159). Outputs (host): logits/probs over the allowed ids (softmax
  * restricted to them) and the argmax index into `allowed` (first maximum). PO_ERR_CAPACITY when
- * n > max_tokens (CapacityError, ps/costs.py:270-274). */
+ * n > max_tokens (CapacityError, ps/costs.py:270-274); PO_ERR_POOL when a slot is out of range or named twice in
+ * one request (an admitted block may not reuse a slot this request reads or admits elsewhere). */
 int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
                int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
                float* out_probs, int32_t* out_argmax, void* stream);
