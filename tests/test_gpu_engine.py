@@ -162,7 +162,10 @@ def test_arena_matches_geometry_model():
     from paper_2505_07203_b200 import geometry
     from paper_2505_07203_b200.config import LLAMA_3_1_8B
 
-    for model, T, chunk in ((TINY, 4096, 1024), (SMALL, 2048, 512), (LLAMA_3_1_8B, 24_000, 8192)):
+    from paper_2505_07203_b200.config import TINY_FP8
+
+    for model, T, chunk in ((TINY, 4096, 1024), (SMALL, 2048, 512), (LLAMA_3_1_8B, 24_000, 8192),
+                            (TINY_FP8, 4096, 1024)):
         with Engine(model, seed=0, max_tokens=T, chunk=chunk, pool_blocks=4) as e:
             assert e.arena_bytes == geometry.arena_bytes(model, T, chunk)
             norms_fp32_extra = (2 * model.num_layers + 1) * model.hidden * 2  # norms held as fp32 on device
