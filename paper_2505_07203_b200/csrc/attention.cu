@@ -59,7 +59,7 @@ struct AttnArgs {
   float scale_log2;
   int splits;         // KV splits per (query block, head pair); 1 = write normalised bf16 output directly
   int tiles_per_split;
-  float* part_o;      // [splits][n_q][hq*128] unnormalised fp32 partial outputs (splits > 1)
+  __nv_bfloat16* part_o;  // [splits][n_q][hq*128] unnormalised partial outputs, bf16 (splits > 1)
   float2* part_ml;    // [splits][n_q][hq] (running max in log2 units, running sum)
   int mode;           // what the two 128-row TMEM slots of a CTA hold (see AttnLayout)
   int R;              // MODE_PACKED: query rows per head in a slot (128 / GQA group)
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
       // split-KV partial: unnormalised O, running max m (log2 units) and sum l for the combine kernel
       const long long prow = (long long)split * a.n_q + row;
-      float4* dst = reinterpret_cast<float4*>(a.part_o + prow * (a.hq * HD) + my_h * HD);
+      uint4* dst = reinterpret_cast<uint4*>(a.part_o + prow * (a.hq * HD) + my_h * HD);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
@@ -511,9 +511,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld_wait();
         if (row < a.n_q) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            dst[c * 8 + q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          for (int q = 0; q < 4; ++q)
+            dst[c * 4 + q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1])),
+                                        pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                                        pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                                        pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
         }
       }
       if (row < a.n_q) a.part_ml[prow * a.hq + my_h] = make_float2(m, l);
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // out[row, h, :] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s over the KV splits that exist for the row's block
-__global__ void attn_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml, int n_q,
+__global__ void attn_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float2* __restrict__ part_ml, int n_q,
                                     int hq, int splits, int tiles_per_split, int q_offset, int n_total, int span,
                                     __nv_bfloat16* __restrict__ out, long long ldo) {
   pdl_wait();
@@ -553,7 +555,10 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o, const floa
       const float2 ml = part_ml[((long long)s * n_q + row) * hq + h];
       const float w = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
       L += w * ml.y;
-      const float4 o = reinterpret_cast<const float4*>(part_o + ((long long)s * n_q + row) * hq * HD + h * HD)[q4];
+      const uint2 ob = reinterpret_cast<const uint2*>(part_o + ((long long)s * n_q + row) * hq * HD + h * HD)[q4];
+      const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ob.x));
+      const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ob.y));
+      const float4 o = make_float4(o01.x, o01.y, o23.x, o23.y);
       acc.x += w * o.x;
       acc.y += w * o.y;
       acc.z += w * o.z;
@@ -623,7 +628,7 @@ size_t attention_workspace_bytes(int n_total, int q_offset, int hq, int hkv) {
   attention_split_plan(n_total, q_offset, hq, hkv, &s, &tps);
   if (s == 1) return 0;
   const size_t n_q = n_total - q_offset;
-  return (size_t)s * n_q * hq * (HD * sizeof(float) + sizeof(float2));
+  return (size_t)s * n_q * hq * (HD * sizeof(__nv_bfloat16) + sizeof(float2));
 }
 
 int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int hq, int hkv, void* out, long long ldo,
@@ -694,16 +699,16 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
     a.tiles_per_split = (n_total - 1) / BKV + 1;
   }
   if (a.splits > 1) {
-    a.part_o = static_cast<float*>(workspace);
+    a.part_o = static_cast<__nv_bfloat16*>(workspace);
     a.part_ml = reinterpret_cast<float2*>(static_cast<char*>(workspace) +
-                                          (size_t)a.splits * a.n_q * hq * HD * sizeof(float));
+                                          (size_t)a.splits * a.n_q * hq * HD * sizeof(__nv_bfloat16));
   }
   const int grid = lay.ctas * a.splits;
   launch_pdl(attn_fwd_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, stream, map, map_q, map_pool, map16, a);
   if (a.splits > 1) {
     const long long total = (long long)a.n_q * hq * (HD / 4);
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-    launch_pdl(attn_combine_kernel, dim3(blocks), dim3(256), 0, stream, (const float*)a.part_o,
+    launch_pdl(attn_combine_kernel, dim3(blocks), dim3(256), 0, stream, (const __nv_bfloat16*)a.part_o,
                (const float2*)a.part_ml, a.n_q, hq, a.splits, a.tiles_per_split, q_offset, n_total, lay.span, a.out,
                ldo);
   }
