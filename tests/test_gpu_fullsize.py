@@ -121,3 +121,21 @@ def test_qwen32b_fp8_10k_properties():
     # carry them to the logits: measured 0.07 / 0.14 here, where the bf16 model of the same shape differs by 0.003 /
     # 0.008 (tools/qwen_hit_probe.py). The bar for FP8 is therefore 0.25 absolute.
     assert (np.abs(hit.logits - cold.logits) <= FP8_HIT_ATOL).all(), (hit.logits, cold.logits)
+
+
+def test_qwen32b_bf16_60k_odd_group_long():
+    """Config 5's longest request on the odd-GQA-group (40/8) attention path with kv-head-banded CTA order:
+    normalised, and a prefix hit agrees with the cold forward within the bf16 logit tolerance."""
+    from paper_2505_07203_b200.config import QWEN_2_5_32B
+
+    n, bt = 60_000, 16
+    toks = tokens_for(6, n)
+    with Engine(QWEN_2_5_32B, seed=0, max_tokens=n, pool_blocks=n // bt + 8) as e:
+        slots = list(range(n // bt))
+        cold = e.prefill(toks, YES_NO, 0, slots)
+        hit = e.prefill(toks, YES_NO, n - 160, slots)
+        aligned = e.prefill(toks, YES_NO, 30_080, slots)
+    print("qwen 60k cold", cold.logits, "hit", hit.logits, "service s", cold.service_s, hit.service_s)
+    assert normalised(cold) and normalised(hit)
+    assert close(hit.logits, cold.logits), (hit.logits, cold.logits)
+    assert np.array_equal(aligned.logits, cold.logits)
