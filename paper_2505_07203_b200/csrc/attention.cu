@@ -649,11 +649,7 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
     map_pool = map;
     map16 = map;
   }
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    configured = true;
-  }
+  ensure_smem_attr<attn_fwd_kernel>(SMEM_BYTES);
   AttnArgs a{};
   a.n_total = n_total;
   a.q_offset = q_offset;

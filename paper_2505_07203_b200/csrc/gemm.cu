@@ -749,11 +749,7 @@ size_t gemm_split_ws_bytes(int M, int N, int K) {
 template <int EPI, int BNT, bool F8 = false>
 static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, const GemmArgs& in,
                          cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm2_kernel<EPI, BNT, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Pair<BNT>::SMEM);
-    configured = true;
-  }
+  ensure_smem_attr<gemm2_kernel<EPI, BNT, F8>>(Pair<BNT>::SMEM);
   GemmArgs args = in;
   args.k_splits = 1;
   const int tiles_mn = ((args.M + 2 * BM - 1) / (2 * BM)) * (args.N / BNT);
@@ -806,11 +802,7 @@ static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, cons
 
 template <int EPI>
 static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmArgs& in, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    configured = true;
-  }
+  ensure_smem_attr<gemm_kernel<EPI>>(SMEM_BYTES);
   GemmArgs args = in;
   args.k_splits = 1;
   if (args.split_ws) {
