@@ -1,6 +1,7 @@
 // extern "C" surface of libprefillonly.so (declared in include/prefillonly.h).
 #include "../../include/prefillonly.h"
 #include "gemm.cuh"
+#include <atomic>
 #include <cstdio>
 #include <string>
 #include <cstdarg>
@@ -20,15 +21,17 @@ int set_error(int code, const char* fmt, ...) {
 // The op entry points take their scratch from the device's default stream-ordered pool. Keep freed blocks in the
 // pool (no release to the driver at every synchronisation), so a per-call workspace costs no driver allocation.
 void keep_pool_memory() {
-  static bool done = false;
-  if (done) return;
+  static std::atomic<uint64_t> done{0};  // one bit per device: each device has its own default pool
   int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
   cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  done = true;
+  done.fetch_or(bit, std::memory_order_acq_rel);
 }
 }  // namespace po
 
