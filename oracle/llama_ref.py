@@ -103,6 +103,27 @@ def init_matrix(seed: int, tid: int, rows: int, cols: int, scale) -> np.ndarray:
     return out
 
 
+class LazyRows:
+    """Rows of a counter-hash bf16 matrix generated on demand (`m[idx]` == init_matrix(...)[idx]), for the vocab-sized
+    embedding / LM head at full model size: a request touches only its token rows and the allowed rows."""
+
+    def __init__(self, seed: int, tid: int, rows: int, cols: int, scale):
+        self.seed, self.tid, self.rows, self.cols, self.scale = seed, tid, rows, cols, np.float32(scale)
+
+    def __getitem__(self, idx) -> np.ndarray:
+        idx = np.atleast_1d(np.asarray(idx, dtype=np.int64))
+        if idx.size and (idx.min() < 0 or idx.max() >= self.rows):
+            raise IndexError("row out of range")
+        out = np.empty((idx.size, self.cols), dtype=np.float32)
+        col = np.arange(self.cols, dtype=np.uint64)
+        step = max(1, (1 << 22) // self.cols)
+        for r0 in range(0, idx.size, step):
+            sel = idx[r0:r0 + step].astype(np.uint64)
+            flat = (sel[:, None] * np.uint64(self.cols) + col[None, :]).ravel()
+            out[r0:r0 + sel.size] = bf16_round(unit_uniform(self.seed, self.tid, flat) * self.scale).reshape(-1, self.cols)
+        return out
+
+
 def init_norm(seed: int, tid: int, n: int) -> np.ndarray:
     u = unit_uniform(seed, tid, np.arange(n, dtype=np.uint64))
     return bf16_round(np.float32(1.0) + np.float32(0.05) * u)
@@ -144,12 +165,15 @@ class Cfg:
         return cls(**{k: getattr(m, k) for k in cls.__dataclass_fields__})
 
 
-def make_weights(cfg: Cfg, seed: int) -> dict:
-    """All weights as float32 arrays holding bf16 values, in the logical (un-interleaved) layout."""
+def make_weights(cfg: Cfg, seed: int, lazy_vocab: bool = False) -> dict:
+    """All weights as float32 arrays holding bf16 values, in the logical (un-interleaved) layout.
+
+    lazy_vocab: the embedding and LM head become LazyRows (same values, generated per indexed row)."""
     h, i_, hd = cfg.hidden, cfg.intermediate, cfg.head_dim
+    mat = LazyRows if lazy_vocab else init_matrix
     w = {
-        "embed": init_matrix(seed, TID_EMBED, cfg.vocab, h, np.float32(1.0)),
-        "lm_head": init_matrix(seed, TID_LM_HEAD, cfg.vocab, h, fan_scale(h)),
+        "embed": mat(seed, TID_EMBED, cfg.vocab, h, np.float32(1.0)),
+        "lm_head": mat(seed, TID_LM_HEAD, cfg.vocab, h, fan_scale(h)),
         "final_norm": init_norm(seed, TID_FINAL_NORM, h),
         "layers": [],
     }

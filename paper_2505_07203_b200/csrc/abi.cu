@@ -62,6 +62,7 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   po::keep_pool_memory();
   const size_t ws = po::gemm_split_ws_bytes(M, N, K);
+  args.split_ws_bytes = ws;
   if (ws && cudaMallocAsync(reinterpret_cast<void**>(&args.split_ws), ws, st) != cudaSuccess)
     return po::set_error(PO_ERR_CUDA, "po_op_gemm: split-K workspace allocation failed");
   rc = po::gemm_run(plan, epi, args, st);
@@ -98,6 +99,7 @@ int po_op_gemm_fp8(const void* A, int64_t lda, const float* a_scale, const void*
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   po::keep_pool_memory();
   const size_t ws = po::gemm_split_ws_bytes_f8(M, N, K);
+  args.split_ws_bytes = ws;
   if (ws && cudaMallocAsync(reinterpret_cast<void**>(&args.split_ws), ws, st) != cudaSuccess)
     return po::set_error(PO_ERR_CUDA, "po_op_gemm_fp8: split-K workspace allocation failed");
   int rc = po::gemm_launch_pair_f8(map_a, map_b, epi, args, st);

@@ -73,8 +73,18 @@ struct po_engine {
   CUtensorMap map_xg8, map_ctx8, map_act8;
   // per-request device staging
   uint32_t* d_tokens = nullptr;
-  int* d_slots = nullptr;
+  int* d_slots = nullptr;   // the current request's ring entry (below)
   int* d_kvslot = nullptr;  // per 16-token block: admission slot in the prefix pool, or -1
+  // Block tables go through a ring of STAGE_RING pinned/device buffer pairs: po_prefill_device returns before its
+  // forward (and the H2D copy of its tables) ran, so the next call must not overwrite those pinned buffers. Each
+  // entry is reused only after the event recorded behind the forward that used it has completed.
+  static constexpr int STAGE_RING = 4;
+  int* ring_h_slots[STAGE_RING] = {};
+  int* ring_h_kvslot[STAGE_RING] = {};
+  int* ring_d_slots[STAGE_RING] = {};
+  int* ring_d_kvslot[STAGE_RING] = {};
+  cudaEvent_t ring_ev[STAGE_RING] = {};
+  int ring_next = 0;
   int* d_allowed = nullptr;
   float* d_logits = nullptr;
   float* d_probs = nullptr;
@@ -166,6 +176,9 @@ int validate_cfg(const po_model_cfg& c) {
   if (c.hidden % 256 || c.intermediate % 128 || ((c.n_heads + 2 * c.n_kv_heads) * 128) % 256)
     return set_error(PO_ERR_CONFIG, "po_init: hidden %% 256, intermediate %% 128 and qkv width %% 256 required");
   if (c.hidden > 8192) return set_error(PO_ERR_CONFIG, "po_init: hidden > 8192 unsupported by the LM-head kernel");
+  // the QKV-epilogue admission (pool_row), pool-direct attention and the pool layout use 16-token blocks
+  if (c.block_tokens != 16)
+    return set_error(PO_ERR_CONFIG, "po_init: block_tokens must be 16 (got %d)", c.block_tokens);
   return 0;
 }
 }  // namespace
@@ -182,8 +195,11 @@ int po_free(po_engine* e) {
   }
   for (void* p : e->allocs) cudaFree(p);
   cudaFreeHost(e->h_tokens);
-  cudaFreeHost(e->h_slots);
-  cudaFreeHost(e->h_kvslot);
+  for (int i = 0; i < po_engine::STAGE_RING; ++i) {
+    cudaFreeHost(e->ring_h_slots[i]);
+    cudaFreeHost(e->ring_h_kvslot[i]);
+    if (e->ring_ev[i]) cudaEventDestroy(e->ring_ev[i]);
+  }
   cudaFreeHost(e->h_allowed);
   cudaFreeHost(e->h_logits);
   cudaFreeHost(e->h_probs);
@@ -342,10 +358,12 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     e->attn_ws_bytes = ws;
     if (ws && dalloc(e, &e->attn_ws, ws, &e->workspace_bytes))
       return fail(PO_ERR_CUDA, "attention workspace failed");
-    // split-K workspace: largest need over the layer GEMM shapes for every M that triggers splitting
+    // split-K workspace: largest need over the layer GEMM shapes for every M (the split count is constant inside a
+    // 128- or 256-row band, so the need peaks at band tops; every M is checked). Launchers also run unsplit when a
+    // plan would exceed split_ws_bytes.
     size_t gw = 0;
     auto ws_of = f8 ? po::gemm_split_ws_bytes_f8 : po::gemm_split_ws_bytes;
-    for (int m = 1; m <= 148 * 128 && m <= T; m += 16) {
+    for (int m = 1; m <= 148 * 256 && m <= T; ++m) {
       gw = std::max(gw, ws_of(m, qkvc, h));
       gw = std::max(gw, ws_of(m, h, ctxc));
       gw = std::max(gw, ws_of(m, 2 * I, h));
@@ -355,16 +373,19 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
   }
   const long long max_blocks = T / c.block_tokens + 1;
+  for (int i = 0; i < po_engine::STAGE_RING; ++i)
+    if (dalloc(e, &e->ring_d_slots[i], (size_t)max_blocks * 4, &e->arena_bytes) ||
+        dalloc(e, &e->ring_d_kvslot[i], (size_t)max_blocks * 4, &e->arena_bytes) ||
+        halloc(&e->ring_h_slots[i], (size_t)max_blocks * 4) || halloc(&e->ring_h_kvslot[i], (size_t)max_blocks * 4) ||
+        cudaEventCreateWithFlags(&e->ring_ev[i], cudaEventDisableTiming) != cudaSuccess)
+      return fail(PO_ERR_CUDA, "staging ring allocation failed");
   if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
-      dalloc(e, &e->d_slots, (size_t)max_blocks * 4, &e->arena_bytes) ||
-      dalloc(e, &e->d_kvslot, (size_t)max_blocks * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_allowed, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_logits, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_probs, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_argmax, 16, &e->arena_bytes))
     return fail(PO_ERR_CUDA, "staging allocation failed");
-  if (halloc(&e->h_tokens, (size_t)T * 4) || halloc(&e->h_slots, (size_t)max_blocks * 4) ||
-      halloc(&e->h_kvslot, (size_t)max_blocks * 4) || halloc(&e->h_allowed, (size_t)c.vocab * 4) ||
+  if (halloc(&e->h_tokens, (size_t)T * 4) || halloc(&e->h_allowed, (size_t)c.vocab * 4) ||
       halloc(&e->h_logits, (size_t)c.vocab * 4) || halloc(&e->h_probs, (size_t)c.vocab * 4) ||
       halloc(&e->h_argmax, 16))
     return fail(PO_ERR_CUDA, "pinned host allocation failed");
@@ -568,6 +589,14 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
   if (n_blocks < 0 || n_blocks > n / bt) return set_error(PO_ERR_ARG, "po_prefill: n_blocks %d > n/bt", n_blocks);
   if (n_cached / bt > n_blocks || (n_blocks > 0 && !pool_block_ids))
     return set_error(PO_ERR_ARG, "po_prefill: cached blocks need pool slots");
+  // next staging-ring entry: wait until the forward that last used it (and its table copies) has completed
+  const int ri = e->ring_next;
+  if (cudaEventSynchronize(e->ring_ev[ri]) != cudaSuccess)
+    return set_error(PO_ERR_CUDA, "po_prefill: an earlier forward failed: %s", cudaGetErrorString(cudaGetLastError()));
+  e->h_slots = e->ring_h_slots[ri];
+  e->h_kvslot = e->ring_h_kvslot[ri];
+  e->d_slots = e->ring_d_slots[ri];
+  e->d_kvslot = e->ring_d_kvslot[ri];
   // a fully cached request still recomputes its last token to produce logits
   const int n_c = n_cached < n ? n_cached : n - 1;
   const int cached_blocks = (n_c + bt - 1) / bt;
@@ -715,7 +744,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.M = n_miss; g.N = qkvc; g.K = h;
     g.out = e->qkv + (size_t)n_c * qkvc; g.ldo = qkvc;
     g.rope = e->rope; g.pos_offset = n_c; g.rope_cols = (c.n_heads + c.n_kv_heads) * c.head_dim;
-    g.split_ws = e->gemm_ws;
+    g.split_ws = e->gemm_ws; g.split_ws_bytes = e->gemm_ws_bytes;
     g.bias = ly.bqkv;
     if (n_admit) {  // suffix-block admission: the QKV epilogue also stores the admitted rows' K/V into the pool
       g.kv_slot = e->d_kvslot; g.kv_pool = e->pool; g.pool_layers = L; g.pool_layer = l;
@@ -744,7 +773,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     ++launches;
     po::GemmArgs go{};
     go.M = rows; go.N = h; go.K = ctxc;
-    go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws;
+    go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws; go.split_ws_bytes = e->gemm_ws_bytes;
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     mark(KC_O, true);
     if (f8)
@@ -757,7 +786,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       const int cr = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
       po::GemmArgs gu{};
       gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
-      gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws;
+      gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws; gu.split_ws_bytes = e->gemm_ws_bytes;
       norm_in(gu, e->ss_mlp + (size_t)lo * nseg);
       mark(KC_GATE_UP, true);
       if (f8)
@@ -767,7 +796,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       mark(KC_GATE_UP, false);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
-      gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws;
+      gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws; gd.split_ws_bytes = e->gemm_ws_bytes;
       norm_out(gd, e->xg + (size_t)lo * h, gamma_next_layer, e->ss_attn + (size_t)lo * nseg);
       mark(KC_DOWN, true);
       if (f8)
@@ -778,6 +807,12 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       launches += f8 ? 4 : 2;
     }
   }
+  // this request's staging-ring entry may be reused once everything enqueued so far has run
+  auto release_ring = [&] {
+    cudaEventRecord(e->ring_ev[e->ring_next], s);
+    e->ring_next = (e->ring_next + 1) % po_engine::STAGE_RING;
+  };
+  if (rc) release_ring();
   if (rc) return set_error(PO_ERR_CUDA, "po_prefill: kernel launch failed (%d): %s", rc,
                            cudaGetErrorString(cudaGetLastError()));
   mark(KC_LM_HEAD, true);
@@ -786,6 +821,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
   mark(KC_LM_HEAD, false);
   ++launches;
   e->last_launches = launches;
+  release_ring();
   if (cudaGetLastError() != cudaSuccess) return set_error(PO_ERR_CUDA, "po_prefill: launch error");
   return PO_OK;
 }

@@ -767,6 +767,7 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
       args.k_splits = s;
       args.kb_per_split = (nk + s - 1) / s;
       args.k_splits = (nk + args.kb_per_split - 1) / args.kb_per_split;
+      if ((size_t)args.k_splits * args.M * args.N * sizeof(float) > args.split_ws_bytes) args.k_splits = 1;
     }
   }
   const int tiles = tiles_mn * args.k_splits;
@@ -808,7 +809,7 @@ static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const Gemm
   if (args.split_ws) {
     int s, kbps;
     split_plan(args.M, args.N, args.K, &s, &kbps);
-    if (s > 1) {
+    if (s > 1 && (size_t)s * args.M * args.N * sizeof(float) <= args.split_ws_bytes) {
       args.k_splits = s;
       args.kb_per_split = kbps;
     }

@@ -41,6 +41,7 @@ struct GemmArgs {
   int k_splits;
   int kb_per_split;
   float* split_ws;
+  size_t split_ws_bytes;  // capacity of split_ws; a launch whose split needs more runs unsplit
   // EPI_QKV_ROPE prefix-pool admission (replaces a separate scatter pass): rows whose 16-token block b (absolute
   // position / 16) has kv_slot[b] >= 0 also store their K/V columns [kv_col0, kv_col0 + kv_dim) into
   // kv_pool[(slot * pool_layers + pool_layer) * 16 + position % 16][kv_dim].

@@ -50,7 +50,8 @@ def arena_bytes(m: ModelConfig, max_tokens: int, chunk: int = DEFAULT_CHUNK) -> 
     if m.weight_fp8:  # E4M3 copies of the GEMM inputs (xg, ctx, act) + their per-row scales
         b += T * h + T * ctx + rows * m.intermediate + 4 * (2 * T + rows)
     max_blocks = T // 16 + 1
-    b += 4 * T + 4 * max_blocks + 4 * max_blocks + 3 * 4 * m.vocab + 16
+    # token ids, a 4-entry ring of (cached-slot, admission-slot) block tables, allowed ids, logits, probs, argmax
+    b += 4 * T + 4 * (4 * max_blocks + 4 * max_blocks) + 3 * 4 * m.vocab + 16
     return b
 
 

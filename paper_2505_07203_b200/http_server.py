@@ -49,6 +49,9 @@ except ImportError:  # pragma: no cover
 def create_app(server):
     from fastapi import FastAPI, HTTPException
 
+    from . import _lib
+    from ._lib import PrefillOnlyError
+
     app = FastAPI(title="prefillonly-b200")
     ids = itertools.count()
     lock = threading.Lock()
@@ -59,10 +62,15 @@ def create_app(server):
             raise HTTPException(400, "need tokens or prompt")
         if not body.allowed:
             raise HTTPException(400, "allowed must be non-empty")
-        toks = np.asarray(body.tokens if body.tokens is not None else list(body.prompt.encode("utf-8")),
-                          dtype=np.uint32)
-        if toks.size == 0:
+        raw = body.tokens if body.tokens is not None else list(body.prompt.encode("utf-8"))
+        if not raw:
             raise HTTPException(400, "empty prompt")
+        if min(raw) < 0 or max(raw) >= 2 ** 32:
+            raise HTTPException(400, "token ids must be in [0, 2^32)")
+        vocab = server.workers[0].engine.model.vocab if hasattr(server.workers[0].engine, "model") else None
+        if min(body.allowed) < 0 or (vocab is not None and max(body.allowed) >= vocab):
+            raise HTTPException(400, f"allowed ids must be in [0, {vocab})")
+        toks = np.asarray(raw, dtype=np.uint32)
         with lock:
             rid = next(ids)
         t0 = time.perf_counter()
@@ -70,6 +78,9 @@ def create_app(server):
             res = server.submit(_HttpRequest(rid, body.user_id, toks), body.allowed).result()
         except ValueError as err:  # CapacityError / ConfigError
             raise HTTPException(413 if "exceeds" in str(err) else 400, str(err)) from None
+        except PrefillOnlyError as err:  # C-ABI status: request errors are the client's, the rest the server's
+            client = err.code in (_lib.PO_ERR_ARG, _lib.PO_ERR_POOL)
+            raise HTTPException(400 if client else 500, str(err)) from None
         return {"id": rid, "token": res.token, "index": res.index, "probs": res.probs.tolist(),
                 "logits": res.logits.tolist(), "n_cached": res.n_cached,
                 "latency_s": time.perf_counter() - t0, "service_s": res.service_s}

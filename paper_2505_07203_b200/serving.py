@@ -223,7 +223,10 @@ class MeasuredServiceFn:
     """Service function that runs each distinct (n_input, n_cached) request shape once on a live Engine and
     reuses the measured device seconds (every shape in the trace is a real forward on the GPU).
 
-    All instances share one engine's measurements (request-level DP replicas on identical GPUs).
+    TIMING ONLY. All instances share one engine's measurements (request-level DP replicas on identical GPUs). A
+    reused measurement runs no forward, so the blocks the loop's cache admitted for that request hold no K/V in the
+    engine's pool, and instances simulated on one engine would name colliding pool slots: the returned token of a
+    reused shape is None, and no pool content produced under this function may be trusted.
     """
 
     def __init__(self, engine, allowed: Sequence[int]):
@@ -237,8 +240,9 @@ class MeasuredServiceFn:
         hit = self.memo.get(key)
         if hit is None:
             res = self.engine.prefill(wr.request.tokens, self.allowed, n_cached, pool_block_ids)
-            hit = self.memo[key] = (res.service_s, res.token)
+            self.memo[key] = (res.service_s, None)
             self.forwards += 1
+            return res.service_s, res.token
         return hit
 
 
@@ -250,6 +254,10 @@ class ReplayServiceFn:
     request in the GPU state the serving order puts it in: a prefix hit right after a cold 20k forward runs at the
     clocks the power cap left (tools/hit_after_cold.py), later hits of the session at recovered clocks. Shapes a
     later run meets that the replay did not (a different cache state) fall back to one measured forward per shape.
+
+    TIMING ONLY once `recording` is off: reused entries run no forward (their admitted pool slots get no K/V) and
+    return token None. Under world > 1 every simulated instance drives this one engine, so their pool slot numbers
+    collide; bench.py's multi-GPU path gives each rank its own engine and shard of the trace instead.
     """
 
     def __init__(self, engine, allowed: Sequence[int]):
@@ -271,10 +279,11 @@ class ReplayServiceFn:
                 hit = (res.service_s, res.token)
                 self.by_shape.setdefault(shape, hit)
             else:
-                hit = self.by_shape[shape]
+                hit = (self.by_shape[shape][0], None)
             if self.recording:
                 self.by_request[key] = hit
-        return hit
+            return hit
+        return hit[0], None
 
 
 def shard_trace(trace, rank: int, world: int):
@@ -432,11 +441,14 @@ class Server:
             self.records.append(rec)
 
     def submit(self, request, allowed: Sequence[int]) -> Future:
-        """Queue one request (duck type .id, .user_id, .n_input, .tokens); resolves to a PrefillResult."""
-        idx = self.router.route(request)
-        bt = self.workers[idx].engine.block_tokens
-        chain = request.digest_chain(bt, self._memo) if hasattr(request, "digest_chain") else \
-            block_chain(request.tokens, bt)
+        """Queue one request (duck type .id, .user_id, .n_input, .tokens); resolves to a PrefillResult.
+
+        Thread-safe: routing (first-seen round robin) and the digest memo are updated under the server lock."""
+        with self._lock:
+            idx = self.router.route(request)
+            bt = self.workers[idx].engine.block_tokens
+            chain = request.digest_chain(bt, self._memo) if hasattr(request, "digest_chain") else \
+                block_chain(request.tokens, bt)
         wr = WaitingRequest(request=request, arrival=self.clock(), chain=chain)
         fut: Future = Future()
         self.workers[idx].enqueue(_Job(wr, tuple(allowed), fut), wr.arrival)

@@ -2,8 +2,8 @@
 
 Bar (north star): allowed-token argmax bit-exact, logits within a stated BF16 tolerance:
     |logit_gpu - logit_oracle| <= LOGIT_ATOL + LOGIT_RTOL * |logit_oracle|
-The argmax must match exactly whenever the oracle's top-2 margin exceeds twice that tolerance (a
-near-tie inside the tolerance band is reported, not silently accepted).
+The argmax must equal the oracle's in every case. The cases use fixed seeds; each test prints the oracle's top-2
+margin, and a case whose margin fell inside the tolerance band would be a failure to decide, not a pass.
 """
 
 import numpy as np
@@ -15,8 +15,8 @@ from paper_2505_07203_b200.engine import CapacityError, Engine
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_ATOL = 2e-2
-LOGIT_RTOL = 2e-2
+LOGIT_ATOL = 1e-2  # measured max |error|: 9e-4 (tiny) .. 7.5e-3 (round 1, all cases)
+LOGIT_RTOL = 5e-3
 YES_NO = [9642, 2822]  # build-chosen "Yes"/"No" ids (Llama-3 tokenizer ids), valid in every preset vocab
 
 SMALL = ModelConfig("small", 2, 1024, 8, 2, 128, 2816, 4096)
@@ -49,8 +49,8 @@ def check_against_oracle(model, res, toks, allowed, seed):
     assert (err <= tol).all(), (res.logits, logits)
     srt = np.sort(logits)[::-1]
     margin = srt[0] - srt[1] if len(srt) > 1 else np.inf
-    if margin > 2 * tol.max():
-        assert res.index == am
+    print(f"  oracle top-2 margin {margin:.3e} (tolerance band {tol.max():.3e})")
+    assert res.index == am, f"argmax {res.index} != oracle {am} (margin {margin:.3e})"
     assert np.allclose(res.probs.sum(), 1.0, atol=1e-5)
 
 
@@ -231,3 +231,36 @@ def test_request_validation_errors(tiny_engine):
     ok = tiny_engine.prefill(toks, [5, 5, 9])  # duplicate allowed ids are legal: equal logits, first max wins
     assert ok.logits[0] == ok.logits[1] and ok.index != 1
     check_against_oracle(TINY, tiny_engine.prefill(toks, YES_NO), toks, YES_NO, 42)
+
+
+def test_back_to_back_async_hits_use_their_own_slot_tables(tiny_engine):
+    """po_prefill_device returns before its forward runs. Two prefix hits issued back to back behind a long cold
+    forward, with different cached slot tables, must each read their own pool slots (the staging ring keeps the
+    first call's block table alive until its forward has consumed it)."""
+    import torch
+
+    bt = 16
+    a, b = tokens_for(41, 1200), tokens_for(42, 1200)
+    slots_a = list(range(0, 75))
+    slots_b = list(range(100, 175))
+    tiny_engine.prefill(a, YES_NO, 0, slots_a)
+    tiny_engine.prefill(b, YES_NO, 0, slots_b)
+    dev = torch.device("cuda", 0)
+    stream = tiny_engine.stream
+    busy = torch.from_numpy(tokens_for(43, 4000).view(np.int32)).to(dev)
+    d_a = torch.from_numpy(a.view(np.int32)).to(dev)
+    d_b = torch.from_numpy(b.view(np.int32)).to(dev)
+    alw = torch.tensor(YES_NO, dtype=torch.int32, device=dev)
+    outs = [(torch.empty(2, device=dev), torch.empty(2, device=dev), torch.empty(1, dtype=torch.int32, device=dev))
+            for _ in range(3)]
+    torch.cuda.synchronize()
+    nc = 1024
+    for (lg, pr, am), d_tok, slots, n_c, n in ((outs[0], busy, [], 0, 4000), (outs[1], d_a, slots_a, nc, 1200),
+                                               (outs[2], d_b, slots_b, nc, 1200)):
+        tiny_engine.prefill_device(d_tok.data_ptr(), n, alw.data_ptr(), 2, lg.data_ptr(), pr.data_ptr(),
+                                   am.data_ptr(), n_cached=n_c, pool_block_ids=slots[: n_c // bt])
+    torch.cuda.synchronize()
+    for (lg, pr, am), toks in ((outs[1], a), (outs[2], b)):
+        res = type("R", (), {})()
+        res.logits, res.probs, res.index = lg.cpu().numpy(), pr.cpu().numpy(), int(am.item())
+        check_against_oracle(TINY, res, toks, YES_NO, 42)

@@ -29,3 +29,15 @@ def test_prefill_endpoint_and_prefix_reuse():
         assert stats["served"] == 3 and stats["cache_hit_requests"] == 1
     finally:
         srv.close()
+
+
+def test_prefill_endpoint_rejects_bad_ids_with_4xx():
+    srv = Server([FakeEngine()], Policy.srjf_calibrated())
+    try:
+        client = TestClient(create_app(srv))
+        assert client.post("/v1/prefill", json={"tokens": [1, -2, 3], "allowed": [5]}).status_code == 400
+        assert client.post("/v1/prefill", json={"tokens": [1, 2 ** 32], "allowed": [5]}).status_code == 400
+        assert client.post("/v1/prefill", json={"tokens": [1, 2], "allowed": [-1]}).status_code == 400
+        assert client.post("/v1/prefill", json={"tokens": [], "allowed": [1]}).status_code == 400
+    finally:
+        srv.close()
