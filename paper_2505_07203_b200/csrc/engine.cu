@@ -18,6 +18,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "attention.cuh"
+#include "stream.cuh"
 #include <cmath>
 #include <cstring>
 #include <cstdio>
@@ -102,6 +103,14 @@ struct po_engine {
   int64_t pool_blocks = 0;
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
+  // persistent weight-streaming kernel (prefix hits): partial tiles, fix-up flags, grid-barrier counter
+  float* stream_ws = nullptr;
+  size_t stream_ws_bytes = 0;
+  uint32_t* stream_flags = nullptr;
+  size_t stream_n_flags = 0;
+  unsigned long long* stream_bar = nullptr;
+  unsigned long long stream_bar_base = 0;
+  uint32_t stream_tag = 1;
   bool act_persist = false;  // the MLP chunk buffer is pinned in L2 (persisting access-policy window)
   std::vector<uint32_t> slot_stamp;  // per pool slot: the last request that named it (collision check)
   uint32_t stamp_gen = 0;
@@ -371,6 +380,22 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     }
     e->gemm_ws_bytes = gw;
     if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
+    if (!f8) {  // streaming kernel (requests of <= 256 miss rows): partials at M = 256 for the four layer GEMMs
+      size_t sw = 0, nf = 0;
+      const int shapes[4][2] = {{qkvc, h}, {h, ctxc}, {2 * I, h}, {h, I}};
+      for (auto& sh : shapes) {
+        sw = std::max(sw, po::stream_ws_bytes(256, sh[0], sh[1]));
+        nf = std::max(nf, po::stream_flag_count(sh[0], sh[1]));
+      }
+      e->stream_ws_bytes = sw;
+      e->stream_n_flags = nf;
+      if (dalloc(e, &e->stream_ws, sw, &e->workspace_bytes) ||
+          dalloc(e, &e->stream_flags, nf * 4, &e->workspace_bytes) ||
+          dalloc(e, &e->stream_bar, 8, &e->workspace_bytes))
+        return fail(PO_ERR_CUDA, "streaming workspace failed");
+      cudaMemsetAsync(e->stream_flags, 0, nf * 4, s);
+      cudaMemsetAsync(e->stream_bar, 0, 8, s);
+    }
   }
   const long long max_blocks = T / c.block_tokens + 1;
   for (int i = 0; i < po_engine::STAGE_RING; ++i)
@@ -680,7 +705,17 @@ bool pool_direct_enabled() {
 }
 
 enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
-              KC_COUNT };
+              KC_STREAM, KC_COUNT };
+
+// PO_STREAM=0 runs prefix hits through the per-GEMM launches instead of the streaming kernel (A/B runs)
+bool stream_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("PO_STREAM");
+    on = (v && v[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
 
 // The hybrid-prefill forward on device-resident inputs; asynchronous on stream s.
 int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admit, const int* d_allowed,
@@ -729,17 +764,46 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     g.xg_out = xg; g.ldxg = h; g.g_next = gamma; g.ss_out = ss; g.ss_nseg = nseg;
   };
   int rc = 0;
-  for (int l = 0; l < L && !rc; ++l) {
-    auto& ly = e->layers[l];
-    const float* gamma_next_layer = l + 1 < L ? e->layers[l + 1].attn_norm : e->final_norm;
-    // cached prefix K/V: read by attention straight from the pool (pool-direct), or gathered into qkv first
-    const bool pool_direct = n_c > 0 && pool_direct_enabled() && bt == 16;
-    if (n_c > 0 && !pool_direct) {
-      mark(KC_GATHER, true);
-      po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
-      mark(KC_GATHER, false);
+  // Prefix hits (n_miss <= 256): the layer GEMMs are weight streams and run as phases of the persistent streaming
+  // kernel (stream.cu), batched O -> gate/up -> down -> next QKV between two attention launches. Larger requests run
+  // one tcgen05 GEMM launch per matrix.
+  const bool streaming = !f8 && n_miss <= 256 && e->stream_ws && stream_enabled();
+  po::StreamArgs sa{};
+  auto flush = [&]() -> int {
+    if (!sa.nph) return 0;
+    sa.ws = e->stream_ws; sa.ws_bytes = e->stream_ws_bytes; sa.flags = e->stream_flags;
+    sa.n_flags = e->stream_n_flags; sa.bar = e->stream_bar; sa.bar_base = e->stream_bar_base; sa.tag = e->stream_tag;
+    mark(KC_STREAM, true);
+    const int r = po::stream_launch(sa, s);
+    mark(KC_STREAM, false);
+    if (!r) {
+      e->stream_bar_base += (unsigned long long)sa.nph * 2 * po::stream_pairs();
+      ++e->stream_tag;
       ++launches;
     }
+    sa.nph = 0;
+    return r;
+  };
+  // one layer GEMM: a streaming phase, or its own launch(es)
+  auto run_gemm = [&](int cls, const CUtensorMap& amap, const void* x, long long ldx, const CUtensorMap& b1,
+                      const CUtensorMap& b2, const CUtensorMap& b3, int epi, const po::GemmArgs& g,
+                      const CUtensorMap& a8, uint8_t* x8, float* xs, const CUtensorMap& bq, const float* bsc) -> int {
+    if (g.M <= 0) return 0;
+    if (streaming) {
+      po::StreamPhase& ph = sa.ph[sa.nph];
+      if (po::make_tmap_a(&ph.a, x, ldx, (long long)g.a_row0 + g.M, g.K)) return -2;
+      ph.b = b2; ph.g = g; ph.epi = epi;
+      return ++sa.nph == po::STREAM_MAX_PHASES ? flush() : 0;
+    }
+    mark(cls, true);
+    int r = f8 ? gemm8(a8, static_cast<const __nv_bfloat16*>(x), ldx, x8, xs, bq, bsc, epi, g, s)
+               : gemm(amap, x, ldx, b1, b2, b3, epi, g, s);
+    mark(cls, false);
+    launches += f8 ? 2 : 1;
+    return r;
+  };
+  auto qkv_gemm = [&](int l) -> int {
+    auto& ly = e->layers[l];
     po::GemmArgs g{};
     g.M = n_miss; g.N = qkvc; g.K = h;
     g.out = e->qkv + (size_t)n_c * qkvc; g.ldo = qkvc;
@@ -751,13 +815,22 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       g.kv_col0 = kv_col0; g.kv_dim = kvd;
     }
     norm_in(g, e->ss_attn);
-    mark(KC_QKV, true);
-    if (f8)
-      rc |= gemm8(e->map_xg8, e->xg, h, e->xg8, e->xg_s, ly.f8_qkv, ly.s_qkv, po::EPI_QKV_ROPE, g, s);
-    else
-      rc |= gemm(e->map_xg, e->xg, h, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g, s);
-    mark(KC_QKV, false);
-    launches += f8 ? 2 : 1;
+    return run_gemm(KC_QKV, e->map_xg, e->xg, h, ly.map_qkv, ly.map2_qkv, ly.map3_qkv, po::EPI_QKV_ROPE, g,
+                    e->map_xg8, e->xg8, e->xg_s, ly.f8_qkv, ly.s_qkv);
+  };
+  rc |= qkv_gemm(0);
+  for (int l = 0; l < L && !rc; ++l) {
+    auto& ly = e->layers[l];
+    const float* gamma_next_layer = l + 1 < L ? e->layers[l + 1].attn_norm : e->final_norm;
+    rc |= flush();  // this layer's QKV (and the previous layer's tail) complete before attention
+    // cached prefix K/V: read by attention straight from the pool (pool-direct), or gathered into qkv first
+    const bool pool_direct = n_c > 0 && pool_direct_enabled() && bt == 16;
+    if (n_c > 0 && !pool_direct) {
+      mark(KC_GATHER, true);
+      po::launch_kv_gather(e->pool, e->d_slots, n_c, l, L, bt, kvd, e->qkv, qkvc, kv_col0, s);
+      mark(KC_GATHER, false);
+      ++launches;
+    }
     // the last layer only needs the final row's output (the LM head reads nothing else); its K/V rows
     // were computed (and admitted to the pool) above
     const bool last_only = c.last_row_only && l == L - 1 && n_miss > 1;
@@ -775,38 +848,26 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     go.M = rows; go.N = h; go.K = ctxc;
     go.resid = e->resid + (size_t)row0 * h; go.ldr = h; go.split_ws = e->gemm_ws; go.split_ws_bytes = e->gemm_ws_bytes;
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
-    mark(KC_O, true);
-    if (f8)
-      rc |= gemm8(e->map_ctx8, e->xn, ctxc, e->ctx8, e->ctx_s, ly.f8_o, ly.s_o, po::EPI_RESID_F32, go, s);
-    else
-      rc |= gemm(e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go, s);
-    mark(KC_O, false);
-    launches += f8 ? 2 : 1;
+    rc |= run_gemm(KC_O, e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go,
+                   e->map_ctx8, e->ctx8, e->ctx_s, ly.f8_o, ly.s_o);
     for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
       const int cr = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
       po::GemmArgs gu{};
       gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws; gu.split_ws_bytes = e->gemm_ws_bytes;
       norm_in(gu, e->ss_mlp + (size_t)lo * nseg);
-      mark(KC_GATE_UP, true);
-      if (f8)
-        rc |= gemm8(e->map_xg8, e->xg, h, e->xg8, e->xg_s, ly.f8_gu, ly.s_gu, po::EPI_SILU_MUL, gu, s);
-      else
-        rc |= gemm(e->map_xg, e->xg, h, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu, s);
-      mark(KC_GATE_UP, false);
+      rc |= run_gemm(KC_GATE_UP, e->map_xg, e->xg, h, ly.map_gu, ly.map2_gu, ly.map3_gu, po::EPI_SILU_MUL, gu,
+                     e->map_xg8, e->xg8, e->xg_s, ly.f8_gu, ly.s_gu);
       po::GemmArgs gd{};
       gd.M = cr; gd.N = h; gd.K = I;
       gd.resid = e->resid + (size_t)lo * h; gd.ldr = h; gd.split_ws = e->gemm_ws; gd.split_ws_bytes = e->gemm_ws_bytes;
       norm_out(gd, e->xg + (size_t)lo * h, gamma_next_layer, e->ss_attn + (size_t)lo * nseg);
-      mark(KC_DOWN, true);
-      if (f8)
-        rc |= gemm8(e->map_act8, e->act, I, e->act8, e->act_s, ly.f8_down, ly.s_down, po::EPI_RESID_F32, gd, s);
-      else
-        rc |= gemm(e->map_act, e->act, I, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd, s);
-      mark(KC_DOWN, false);
-      launches += f8 ? 4 : 2;
+      rc |= run_gemm(KC_DOWN, e->map_act, e->act, I, ly.map_down, ly.map2_down, ly.map3_down, po::EPI_RESID_F32, gd,
+                     e->map_act8, e->act8, e->act_s, ly.f8_down, ly.s_down);
     }
+    if (l + 1 < L) rc |= qkv_gemm(l + 1);
   }
+  rc |= flush();
   // this request's staging-ring entry may be reused once everything enqueued so far has run
   auto release_ring = [&] {
     cudaEventRecord(e->ring_ev[e->ring_next], s);

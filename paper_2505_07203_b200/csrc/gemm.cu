@@ -7,6 +7,7 @@
 //   warps 4..7  epilogue: tcgen05.ld 32 rows x 32 columns per warp, fused op, global store
 // Pipelines: smem full/empty ring (TMA <-> MMA) and TMEM full/empty pair (MMA <-> epilogue).
 #include "gemm.cuh"
+#include "gemm_epi.cuh"
 #include <cuda_fp8.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -35,219 +36,6 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& m_
   const int local = t - g * per_group;
   m_blk = first_m + local % gsz;
   n_blk = local / gsz;
-}
-
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
-
-// 1/rms of output row `row` from the producer's per-segment sums of squares (fixed summation order; the loads go
-// out 8 at a time so their latency is paid once per 8 segments, not once per segment)
-__device__ __forceinline__ float row_inv_rms(const GemmArgs& a, int row) {
-  const float* p = a.ss_in + (long long)row * a.ss_nseg;
-  float s = 0.f;
-  for (int i0 = 0; i0 < a.ss_nseg; i0 += 8) {
-    float x[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = i0 + i < a.ss_nseg ? p[i0 + i] : 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i0 + i < a.ss_nseg) s += x[i];
-  }
-  return rsqrtf(s / a.norm_dim + a.norm_eps);
-}
-
-// Prefix-pool row (offset so that column index col addresses it) of output row `row` when its block is admitted
-// and the column block [hcol, hcol + 128) holds K or V; null otherwise (see GemmArgs::kv_slot).
-__device__ __forceinline__ __nv_bfloat16* pool_row(const GemmArgs& a, int row, int hcol) {
-  if (!a.kv_pool || hcol < a.kv_col0) return nullptr;
-  const int pos = a.pos_offset + row;
-  const int slot = a.kv_slot[pos >> 4];
-  if (slot < 0) return nullptr;
-  return a.kv_pool + (((long long)slot * a.pool_layers + a.pool_layer) * 16 + (pos & 15)) * a.kv_dim - a.kv_col0;
-}
-__device__ __forceinline__ void store_bf16_32(__nv_bfloat16* dst, const uint32_t (&r)[32]) {
-  uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    d[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1])),
-                      pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3])),
-                      pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5])),
-                      pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
-}
-
-template <int EPI>
-__device__ __forceinline__ float epilogue_chunk(const GemmArgs& a, int row, int col0, const uint32_t (&r)[32],
-                                                float sc = 1.0f) {
-  float sq = 0.f;
-  if constexpr (EPI == EPI_BF16) {
-    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 v;
-      v.x = pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1]));
-      v.y = pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
-      v.z = pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
-      v.w = pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
-      dst[q] = v;
-    }
-  } else if constexpr (EPI == EPI_F32) {
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.out) + (long long)row * a.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                           __uint_as_float(r[4 * q + 3]));
-  } else if constexpr (EPI == EPI_RESID_F32) {
-    float4* dst = reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col0);
-    float4 v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = dst[q];  // all loads in flight first
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      v[q].x += __uint_as_float(r[4 * q + 0]);
-      v[q].y += __uint_as_float(r[4 * q + 1]);
-      v[q].z += __uint_as_float(r[4 * q + 2]);
-      v[q].w += __uint_as_float(r[4 * q + 3]);
-      dst[q] = v[q];
-    }
-    if (a.xg_out) {
-      const float4* g4 = reinterpret_cast<const float4*>(a.g_next + col0);
-      uint4* xo = reinterpret_cast<uint4*>(a.xg_out + (long long)row * a.ldxg + col0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 ga = g4[2 * q], gb = g4[2 * q + 1];
-        const float4 va = v[2 * q], vb = v[2 * q + 1];
-        xo[q] = make_uint4(pack_bf16(va.x * ga.x, va.y * ga.y), pack_bf16(va.z * ga.z, va.w * ga.w),
-                           pack_bf16(vb.x * gb.x, vb.y * gb.y), pack_bf16(vb.z * gb.z, vb.w * gb.w));
-        sq += va.x * va.x + va.y * va.y + va.z * va.z + va.w * va.w + vb.x * vb.x + vb.y * vb.y + vb.z * vb.z +
-              vb.w * vb.w;
-      }
-    }
-  } else if constexpr (EPI == EPI_SILU_MUL) {
-    // 32 accumulator columns = 16 gate columns followed by the matching 16 up columns; sc = this row's 1/rms
-    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col0 / 2);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = 8 * q + 2 * e;
-        const float x0 = silu_f(sc * __uint_as_float(r[j])) * (sc * __uint_as_float(r[16 + j]));
-        const float x1 = silu_f(sc * __uint_as_float(r[j + 1])) * (sc * __uint_as_float(r[16 + j + 1]));
-        w[e] = pack_bf16(x0, x1);
-      }
-      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-  }
-  return sq;
-}
-
-// FP8: dequantise 32 accumulator columns [col0, col0 + 32) of this row: acc * a_scale[row] * b_scale[col]
-template <bool F8>
-__device__ __forceinline__ void dequant32(const GemmArgs& a, float as, int col0, uint32_t (&r)[32]) {
-  if constexpr (F8) {
-    const float4* b4 = reinterpret_cast<const float4*>(a.b_scale + col0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 b = __ldg(b4 + q);
-      r[4 * q + 0] = __float_as_uint(__uint_as_float(r[4 * q + 0]) * as * b.x);
-      r[4 * q + 1] = __float_as_uint(__uint_as_float(r[4 * q + 1]) * as * b.y);
-      r[4 * q + 2] = __float_as_uint(__uint_as_float(r[4 * q + 2]) * as * b.z);
-      r[4 * q + 3] = __float_as_uint(__uint_as_float(r[4 * q + 3]) * as * b.w);
-    }
-  }
-}
-
-// Epilogue of one 128-row x 256-column accumulator (this thread: TMEM lane = output row `row`).
-template <int EPI, int BNT = BN, bool F8 = false>
-__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t taddr, int row, int nb, int ksp, int t) {
-  const float as = (F8 && row < args.M) ? args.a_scale[row] : 0.f;
-  if (ksp > 1) {
-    // split-K partial: raw fp32 tile into the workspace slice of this split
-    GemmArgs pa = args;
-    pa.out = args.split_ws + (size_t)(t % ksp) * args.M * args.N;
-    pa.ldo = args.N;
-#pragma unroll 1
-    for (int c = 0; c < BNT; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait();
-      if (row < args.M) epilogue_chunk<EPI_F32>(pa, row, nb * BNT + c, r);
-    }
-  } else if constexpr (EPI == EPI_QKV_ROPE) {
-    // two 128-column heads per tile; rotate-half pairs (i, i+64)
-    const float sc = (args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
-#pragma unroll 1
-    for (int h = 0; h < BNT / 128; ++h) {
-      const int hcol = nb * BNT + h * 128;
-      const bool rot = hcol < args.rope_cols;
-      const float2* cs = args.rope + (long long)(args.pos_offset + row) * 64;
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        uint32_t x1[32], x2[32];
-        tmem_ld32(taddr + h * 128 + half * 32, x1);
-        tmem_ld32(taddr + h * 128 + 64 + half * 32, x2);
-        tmem_ld_wait();
-        dequant32<F8>(args, as, hcol + half * 32, x1);
-        dequant32<F8>(args, as, hcol + 64 + half * 32, x2);
-        if (args.ss_in) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            x1[i] = __float_as_uint(sc * __uint_as_float(x1[i]));
-            x2[i] = __float_as_uint(sc * __uint_as_float(x2[i]));
-          }
-        }
-        if (args.bias) {
-          const float* b1 = args.bias + hcol + half * 32;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            x1[i] = __float_as_uint(__uint_as_float(x1[i]) + b1[i]);
-            x2[i] = __float_as_uint(__uint_as_float(x2[i]) + b1[64 + i]);
-          }
-        }
-        if (row < args.M) {
-          if (rot) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float2 c = cs[half * 32 + i];
-              const float a0 = __uint_as_float(x1[i]);
-              const float b0 = __uint_as_float(x2[i]);
-              x1[i] = __float_as_uint(a0 * c.x - b0 * c.y);
-              x2[i] = __float_as_uint(b0 * c.x + a0 * c.y);
-            }
-          }
-          epilogue_chunk<EPI_BF16>(args, row, hcol + half * 32, x1);
-          epilogue_chunk<EPI_BF16>(args, row, hcol + 64 + half * 32, x2);
-          if (__nv_bfloat16* prow = pool_row(args, row, hcol)) {
-            store_bf16_32(prow + hcol + half * 32, x1);
-            store_bf16_32(prow + hcol + 64 + half * 32, x2);
-          }
-        }
-      }
-    }
-  } else if constexpr (EPI == EPI_RESID_F32) {
-    float sq[2] = {0.f, 0.f};
-#pragma unroll 1
-    for (int c = 0; c < BNT; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait();
-      dequant32<F8>(args, as, nb * BNT + c, r);
-      if (row < args.M) sq[c >> 7] += epilogue_chunk<EPI>(args, row, nb * BNT + c, r);
-    }
-    if (args.ss_out && row < args.M) {
-#pragma unroll
-      for (int k = 0; k < BNT / 128; ++k) args.ss_out[(long long)row * args.ss_nseg + nb * (BNT / 128) + k] = sq[k];
-    }
-  } else {
-    const float sc = (EPI == EPI_SILU_MUL && args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
-#pragma unroll 1
-    for (int c = 0; c < BNT; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait();
-      dequant32<F8>(args, as, nb * BNT + c, r);
-      if (row < args.M) epilogue_chunk<EPI>(args, row, nb * BNT + c, r, sc);
-    }
-  }
 }
 
 template <int EPI>

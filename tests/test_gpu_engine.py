@@ -264,3 +264,33 @@ def test_back_to_back_async_hits_use_their_own_slot_tables(tiny_engine):
         res = type("R", (), {})()
         res.logits, res.probs, res.index = lg.cpu().numpy(), pr.cpu().numpy(), int(am.item())
         check_against_oracle(TINY, res, toks, YES_NO, 42)
+
+
+@pytest.fixture(scope="module")
+def small_engine():
+    with Engine(SMALL, seed=7, max_tokens=2048, chunk=1024, pool_blocks=256) as e:
+        yield e
+
+
+@pytest.mark.parametrize("n", [1, 100, 128, 129, 200, 256])
+def test_streaming_kernel_short_requests_match_oracle(small_engine, n):
+    """Requests of <= 256 miss rows run their layer GEMMs as phases of the persistent weight-streaming kernel
+    (stream.cu: stream-K split of every weight matrix over the SM pairs, in-kernel fix-up, grid barriers between the
+    O / gate-up / down / next-QKV phases). M = 1 leaves the second CTA of each pair without rows; 129 crosses it."""
+    toks = tokens_for(50 + n, n)
+    res = small_engine.prefill(toks, [5, 11, 4095])
+    check_against_oracle(SMALL, res, toks, [5, 11, 4095], 7)
+
+
+def test_streaming_kernel_hit_suffixes_match_oracle(small_engine):
+    """Prefix hits with 160- and 256-row suffixes (the serving hot path) and admission from the streamed QKV phase."""
+    base = tokens_for(60, 1600)
+    slots = list(range(0, 100))
+    small_engine.prefill(base[:1344], [5, 11, 4095], 0, slots[:84])
+    for n_cached, n in ((1344, 1504), (1344, 1600)):
+        toks = base[:n]
+        res = small_engine.prefill(toks, [5, 11, 4095], n_cached, slots[: n // 16])
+        check_against_oracle(SMALL, res, toks, [5, 11, 4095], 7)
+    # blocks 84..99 were admitted by the streamed QKV epilogue of the second hit: serve them as cached keys
+    res = small_engine.prefill(base, [5, 11, 4095], 1584, slots)
+    check_against_oracle(SMALL, res, base, [5, 11, 4095], 7)
