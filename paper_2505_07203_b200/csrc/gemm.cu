@@ -313,36 +313,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-// Split-K reduction: sum the partials in split order, then apply the epilogue (one thread per 4 columns).
-// Sum of the k-split partials at p, p + slice, ... in split order; all loads issued before the adds.
-__device__ __forceinline__ float4 split_sum(const float* p, size_t slice, int splits) {
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s0 = 0; s0 < splits; s0 += 8) {
-    float4 v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      v[k] = s0 + k < splits ? __ldcg(reinterpret_cast<const float4*>(p + (s0 + k) * slice)) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (s0 + k < splits) {
-        acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
-      }
-    }
-  }
-  return acc;
-}
-
-// FP8 split-K: dequantise a summed 4-column group (same order as dequant32: (acc * a_scale) * b_scale)
-__device__ __forceinline__ void dq4(const GemmArgs& a, int row, int col, float4& v) {
-  if (!a.b_scale) return;
-  const float as = a.a_scale[row];
-  const float4 b = *reinterpret_cast<const float4*>(a.b_scale + col);
-  v.x = v.x * as * b.x;
-  v.y = v.y * as * b.y;
-  v.z = v.z * as * b.z;
-  v.w = v.w * as * b.w;
-}
-
 template <int EPI>
 __global__ void splitk_reduce_kernel(const GemmArgs a) {
   pdl_wait();
@@ -354,78 +324,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
        i += (long long)gridDim.x * blockDim.x) {
     const int row = static_cast<int>(i / ncol4);
     const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
-    const float* p = a.split_ws + (size_t)row * a.N + col;
-    float4 acc = split_sum(p, slice, a.k_splits);
-    dq4(a, row, col, acc);
-    float sc = 1.0f;
-    if constexpr (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
-      if (a.ss_in) sc = row_inv_rms(a, row);
-      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
-    }
-    if constexpr (EPI == EPI_BF16) {
-      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
-          make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
-    } else if constexpr (EPI == EPI_F32) {
-      *reinterpret_cast<float4*>(static_cast<float*>(a.out) + (long long)row * a.ldo + col) = acc;
-    } else if constexpr (EPI == EPI_RESID_F32) {
-      float4* d = reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col);
-      float4 v = *d;
-      v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
-      *d = v;
-      if (a.xg_out) {
-        // N % 128 == 0: each warp covers one 128-column segment of one row (warps stay converged)
-        const float4 g = *reinterpret_cast<const float4*>(a.g_next + col);
-        *reinterpret_cast<uint2*>(a.xg_out + (long long)row * a.ldxg + col) =
-            make_uint2(pack_bf16(v.x * g.x, v.y * g.y), pack_bf16(v.z * g.z, v.w * g.w));
-        float sq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if ((threadIdx.x & 31) == 0) a.ss_out[(long long)row * a.ss_nseg + col / 128] = sq;
-      }
-    } else if constexpr (EPI == EPI_SILU_MUL) {
-      // 16-column groups: [gate 16 | up 16]; this thread's 4 columns are gate or up of output cols
-      const int grp = col / 32, w = col % 32;
-      if (w < 16) {
-        float4 up = split_sum(p + 16, slice, a.k_splits);
-        dq4(a, row, col + 16, up);
-        up.x *= sc; up.y *= sc; up.z *= sc; up.w *= sc;
-        const int oc = grp * 16 + w;
-        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
-            make_uint2(pack_bf16(silu_f(acc.x) * up.x, silu_f(acc.y) * up.y),
-                       pack_bf16(silu_f(acc.z) * up.z, silu_f(acc.w) * up.w));
-      }
-    } else if constexpr (EPI == EPI_QKV_ROPE) {
-      const int head_col = col % 128;
-      if (a.bias) {
-        acc.x += a.bias[col]; acc.y += a.bias[col + 1]; acc.z += a.bias[col + 2]; acc.w += a.bias[col + 3];
-      }
-      if (col < a.rope_cols && head_col < 64) {
-        float4 x2 = split_sum(p + 64, slice, a.k_splits);
-        dq4(a, row, col + 64, x2);
-        x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
-        if (a.bias) {
-          x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
-        }
-        const float2* cs = a.rope + (long long)(a.pos_offset + row) * 64 + head_col;
-        const float4 x1 = acc;
-        const float2 c0 = cs[0], c1 = cs[1], c2 = cs[2], c3 = cs[3];
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col;
-        const uint2 lo = make_uint2(pack_bf16(x1.x * c0.x - x2.x * c0.y, x1.y * c1.x - x2.y * c1.y),
-                                    pack_bf16(x1.z * c2.x - x2.z * c2.y, x1.w * c3.x - x2.w * c3.y));
-        const uint2 hi = make_uint2(pack_bf16(x2.x * c0.x + x1.x * c0.y, x2.y * c1.x + x1.y * c1.y),
-                                    pack_bf16(x2.z * c2.x + x1.z * c2.y, x2.w * c3.x + x1.w * c3.y));
-        *reinterpret_cast<uint2*>(o) = lo;
-        *reinterpret_cast<uint2*>(o + 64) = hi;
-        if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) {
-          *reinterpret_cast<uint2*>(prow + col) = lo;
-          *reinterpret_cast<uint2*>(prow + col + 64) = hi;
-        }
-      } else if (col >= a.rope_cols) {
-        const uint2 v = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
-        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) = v;
-        if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) *reinterpret_cast<uint2*>(prow + col) = v;
-      }
-    }
+    splitk_reduce_quad<EPI>(a, row, col, a.split_ws + (size_t)row * a.N + col, slice, a.k_splits);
   }
 }
 

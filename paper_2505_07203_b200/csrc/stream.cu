@@ -4,7 +4,8 @@
 //   warp 0      TMA producer (one lane): per k-block its CTA's 128 activation rows + 128 of the 256 weight rows
 //   warp 1      MMA issuer (leader CTA, one lane): tcgen05.mma.cta_group::2 M256 N256 K16 into a TMEM accumulator
 //   warp 2      TMEM allocator (2 x 256 columns, double buffered across units and phases)
-//   warps 4..7  epilogue: fp32 partial dump + flag, or flag wait + partial add + fused epilogue; grid-barrier arrival
+//   warps 4..7  epilogue: fused epilogue from TMEM, or fp32 partial dump + flag and the cooperative fix-up of the
+//               split tiles; grid-barrier arrival after each phase
 #include "stream.cuh"
 #include "gemm_epi.cuh"
 
@@ -21,32 +22,39 @@ constexpr int SMEM = STAGES * STAGE + 1024 + 256;
 constexpr int NT = 256;
 
 struct Geo {
-  int nk, ntiles, spt, M;
+  int nk, ntiles, spt, M, P;  // P: pairs with work (min(pairs, W): every one of them owns >= 1 k-block)
   long long W;
 };
-__device__ __forceinline__ Geo geo_of(const StreamPhase& p) {
+__device__ __forceinline__ Geo geo_of(const StreamPhase& p, int pairs) {
   Geo g;
   g.nk = p.g.K / BK;
   g.ntiles = p.g.N / BN;
   g.W = (long long)g.nk * g.ntiles;
+  g.P = g.W < pairs ? (int)g.W : pairs;
   g.spt = p.slots_per_tile;
   g.M = p.g.M;
   return g;
+}
+__device__ __forceinline__ int range_lo(const Geo& g, int pair) {
+  return pair < g.P ? stream_pair_start(g.W, g.P, pair) : (int)g.W;
+}
+__device__ __forceinline__ int range_hi(const Geo& g, int pair) {
+  return pair < g.P ? stream_pair_start(g.W, g.P, pair + 1) : (int)g.W;
 }
 struct Unit {
   int tile, kb0, kb1, seg, nseg;
 };
 // The unit of pair `pair` that starts at global k-block kb (ends at its range end or the tile end).
-__device__ __forceinline__ Unit unit_at(const Geo& g, int P, int pair, int kb) {
+__device__ __forceinline__ Unit unit_at(const Geo& g, int pair, int kb) {
   Unit u;
   u.tile = kb / g.nk;
   const int t0 = u.tile * g.nk;
-  const int end = min(stream_pair_start(g.W, P, pair + 1), t0 + g.nk);
+  const int end = min(range_hi(g, pair), t0 + g.nk);
   u.kb0 = kb - t0;
   u.kb1 = end - t0;
-  const int first = stream_owner(g.W, P, t0);
+  const int first = stream_owner(g.W, g.P, t0);
   u.seg = pair - first;
-  u.nseg = stream_owner(g.W, P, t0 + g.nk - 1) - first + 1;
+  u.nseg = stream_owner(g.W, g.P, t0 + g.nk - 1) - first + 1;
   return u;
 }
 
@@ -66,11 +74,6 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 // generic-proxy writes of other CTAs (epilogue stores) -> this CTA's async-proxy reads (TMA), and the reverse
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-template <int EPI>
-__device__ __forceinline__ void fixup_epilogue(const StreamPhase& P, uint32_t taddr, int row, const Unit& u,
-                                               const PartSrc& ps) {
-  epilogue_tile<EPI, BN, false, true>(P.g, taddr, row, u.tile, 1, 0, ps);
-}
 }  // namespace
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel(const __grid_constant__ StreamArgs A) {
@@ -123,8 +126,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
       uint32_t ph = 0;
       for (int f = 0; f < A.nph; ++f) {
         const StreamPhase& F = A.ph[f];
-        const Geo g = geo_of(F);
-        const int lo = stream_pair_start(g.W, P, pair), hi = stream_pair_start(g.W, P, pair + 1);
+        const Geo g = geo_of(F, P);
+        const int lo = range_lo(g, pair), hi = range_hi(g, pair);
         int pend_s[STAGES], pend_k[STAGES];
         int npend = 0;
         bool open = false;
@@ -169,10 +172,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
       uint32_t ph = 0;
       int it = 0;
       for (int f = 0; f < A.nph; ++f) {
-        const Geo g = geo_of(A.ph[f]);
-        const int hi = stream_pair_start(g.W, P, pair + 1);
-        for (int kb = stream_pair_start(g.W, P, pair); kb < hi; ++it) {
-          const Unit u = unit_at(g, P, pair, kb);
+        const Geo g = geo_of(A.ph[f], P);
+        const int hi = range_hi(g, pair);
+        for (int kb = range_lo(g, pair); kb < hi; ++it) {
+          const Unit u = unit_at(g, pair, kb);
           const int acc = it & 1;
           const uint32_t acc_ph = (it >> 1) & 1;
           mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
@@ -197,27 +200,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
     __syncwarp();
   } else if (warp >= 4) {
     const int wq = warp & 3;
+    const int et = threadIdx.x - 128;  // 0..127 within the epilogue warps
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
-    const int row = rank * BM + wq * 32 + lane;  // output row of this thread (single 256-row m tile)
+    const int row = rank * BM + wq * 32 + lane;  // accumulator row of this thread (single 256-row m tile)
     int it = 0;
     for (int f = 0; f < A.nph; ++f) {
       const StreamPhase& F = A.ph[f];
-      const Geo g = geo_of(F);
+      const Geo g = geo_of(F, P);
       const uint32_t tag = A.tag * 8u + (uint32_t)f;
-      const int hi = stream_pair_start(g.W, P, pair + 1);
-      for (int kb = stream_pair_start(g.W, P, pair); kb < hi; ++it) {
-        const Unit u = unit_at(g, P, pair, kb);
+      const long long slot_elems = (long long)g.M * BN;
+      int split_tiles[2], nsplit = 0;
+      const int hi = range_hi(g, pair);
+      for (int kb = range_lo(g, pair); kb < hi; ++it) {
+        const Unit u = unit_at(g, pair, kb);
         kb += u.kb1 - u.kb0;
         const int acc = it & 1;
         const uint32_t acc_ph = (it >> 1) & 1;
         mbar_wait(&tfull_bar[acc], acc_ph);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-        const long long slot0 = (long long)u.tile * g.spt;  // this tile's first partial slot (segment 1)
-        const long long slot_elems = (long long)g.M * BN;
-        if (u.seg > 0) {
-          // a later k segment of a tile owned by an earlier pair: dump the fp32 partial, then raise its flag
-          float* dst = A.ws + (slot0 + u.seg - 1) * slot_elems + (long long)row * BN;
+        if (u.nseg > 1) {
+          // a tile cut across pairs: dump this segment's fp32 partial and raise its flag; the segments' owners
+          // reduce the tile together once all are in (below)
+          const long long slot = (long long)u.tile * g.spt + u.seg;
+          float* dst = A.ws + slot * slot_elems + (long long)row * BN;
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
@@ -233,34 +239,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
           }
           tc_fence_before();
           named_bar_sync(1, 128);
-          if (threadIdx.x == 128) {
+          if (et == 0) {
             mbar_arrive_cluster(tempty0 + acc * 8);
             __threadfence();
-            st_release_u32(A.flags + (slot0 + u.seg - 1) * 2 + rank, tag);
+            st_release_u32(A.flags + slot * 2 + rank, tag);
           }
+          split_tiles[nsplit++] = u.tile;
         } else {
-          if (u.nseg > 1) {
-            // the tile's later segments were the first units of the following pairs: wait for their flags
-            if (threadIdx.x == 128)
-              for (int j = 1; j < u.nseg; ++j)
-                while (ld_acquire_u32(A.flags + (slot0 + j - 1) * 2 + rank) != tag) __nanosleep(32);
-            named_bar_sync(2, 128);
-          }
-          const PartSrc ps{A.ws + slot0 * slot_elems, u.nseg - 1, slot_elems, BN};
+          // a whole tile in one unit: fused epilogue straight from TMEM
           switch (F.epi) {
-            case EPI_RESID_F32: fixup_epilogue<EPI_RESID_F32>(F, taddr, row, u, ps); break;
-            case EPI_SILU_MUL: fixup_epilogue<EPI_SILU_MUL>(F, taddr, row, u, ps); break;
-            case EPI_QKV_ROPE: fixup_epilogue<EPI_QKV_ROPE>(F, taddr, row, u, ps); break;
-            default: fixup_epilogue<EPI_BF16>(F, taddr, row, u, ps); break;
+            case EPI_RESID_F32: epilogue_tile<EPI_RESID_F32, BN>(F.g, taddr, row, u.tile, 1, 0); break;
+            case EPI_SILU_MUL: epilogue_tile<EPI_SILU_MUL, BN>(F.g, taddr, row, u.tile, 1, 0); break;
+            case EPI_QKV_ROPE: epilogue_tile<EPI_QKV_ROPE, BN>(F.g, taddr, row, u.tile, 1, 0); break;
+            default: epilogue_tile<EPI_BF16, BN>(F.g, taddr, row, u.tile, 1, 0); break;
           }
           tc_fence_before();
           named_bar_sync(1, 128);
-          if (threadIdx.x == 128) mbar_arrive_cluster(tempty0 + acc * 8);
+          if (et == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+        }
+      }
+      // cooperative fix-up of the split tiles this pair holds a segment of (at most two: its first and last unit):
+      // the tile's 2 x nseg CTAs each sum every segment for an interleaved share of its rows, in segment order
+      for (int i = 0; i < nsplit; ++i) {
+        const int t = split_tiles[i];
+        const int q0 = stream_owner(g.W, g.P, t * g.nk);
+        const int nseg = stream_owner(g.W, g.P, t * g.nk + g.nk - 1) - q0 + 1;
+        const long long slot0 = (long long)t * g.spt;
+        if (et == 0) {
+          const int ranks = g.M > BM ? 2 : 1;  // a CTA with no rows below M dumps nothing but still flags
+          for (int j = 0; j < nseg; ++j)
+            for (int r = 0; r < ranks; ++r)
+              while (ld_acquire_u32(A.flags + (slot0 + j) * 2 + r) != tag) __nanosleep(32);
+        }
+        named_bar_sync(2, 128);
+        const int workers = 2 * nseg, worker = 2 * (pair - q0) + rank;
+        const int sub = et >> 6, c = (et & 63) * 4;  // two rows per pass; each warp one 128-column segment
+        const float* base = A.ws + slot0 * slot_elems + c;
+        for (int rr = 2 * worker + sub; rr < g.M; rr += 2 * workers) {
+          const float* p = base + (long long)rr * BN;
+          switch (F.epi) {
+            case EPI_RESID_F32: splitk_reduce_quad<EPI_RESID_F32>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
+            case EPI_SILU_MUL: splitk_reduce_quad<EPI_SILU_MUL>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
+            case EPI_QKV_ROPE: splitk_reduce_quad<EPI_QKV_ROPE>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
+            default: splitk_reduce_quad<EPI_BF16>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
+          }
         }
       }
       // this CTA's outputs of phase f are stored: arrive on the grid barrier
       named_bar_sync(1, 128);
-      if (threadIdx.x == 128) {
+      if (et == 0) {
         fence_proxy_async_global();
         __threadfence();
         atomicAdd(A.bar, 1ull);
@@ -280,16 +307,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
 // ------------------------------------------------------------------ host side
 int stream_pairs() { return num_sms() / 2; }
 
+// partial slots per tile: every segment of a split tile dumps (0 when no tile is split)
 static int slots_per_tile(int N, int K) {
-  const int P = stream_pairs();
   const int nk = K / BK, ntiles = N / BN;
   const long long W = (long long)nk * ntiles;
+  const int P = W < stream_pairs() ? (int)W : stream_pairs();
   int most = 1;
   for (int t = 0; t < ntiles; ++t) {
     const int nseg = stream_owner(W, P, (t + 1) * nk - 1) - stream_owner(W, P, t * nk) + 1;
     most = nseg > most ? nseg : most;
   }
-  return most - 1;
+  return most > 1 ? most : 0;
 }
 
 size_t stream_ws_bytes(int M, int N, int K) { return (size_t)(N / BN) * slots_per_tile(N, K) * M * BN * sizeof(float); }

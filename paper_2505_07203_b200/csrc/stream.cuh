@@ -6,9 +6,12 @@
 // STREAM_MAX_PHASES dependent GEMMs of a layer (O-proj -> gate/up -> down -> next layer's QKV) as phases:
 //   * work split: each phase's (weight tile, k-block) space is cut into equal contiguous ranges, one per CTA pair
 //     (stream-K), so every pair streams the same number of weight bytes in every phase;
-//   * fix-up: a tile cut across pairs has its first k segment processed LAST by its owner pair and its other segments
-//     FIRST by the following pairs (which dump fp32 partials and raise a flag); the owner adds them in segment order
-//     to its TMEM accumulator and runs the fused epilogue, so no reduce launch exists and the sum order is fixed;
+//   * fix-up: a tile that lies inside one pair's range gets its fused epilogue straight from TMEM. A tile cut across
+//     pairs is cut at most at its ends of each pair's range, so its segments are the last unit of one pair and the
+//     first units of the next ones: each segment dumps its fp32 partial and raises a flag, and once a pair has dumped
+//     all its units the tile's 2 x nseg CTAs sum all segments (in segment order) for interleaved shares of the rows
+//     and run the fused epilogue. No reduce launch exists, the work is spread over the tile's owners, and the
+//     summation order is fixed;
 //   * phases are separated by a grid barrier (one counter, monotonic across launches); before waiting on it the TMA
 //     producer already streams the next phase's first weight k-blocks into the free stages (weights do not depend on
 //     the previous phase), so the DRAM pipe stays busy across the barrier.
