@@ -59,6 +59,15 @@ int po_op_gemm_fp8(const void* A, int64_t lda, const float* a_scale, const void*
                    int32_t K, int32_t epi, const void* rope_table, int32_t pos_offset, int32_t rope_cols,
                    void* stream);
 
+/* A chain of one or two GEMMs through the persistent weight-streaming kernel that runs prefix hits' layer GEMMs
+ * (M <= 256 rows; stream-K split of the weight matrix over the SM pairs, in-kernel fix-up, grid barrier between the
+ * phases): out1(bf16)[M,N1] = A[M,K] . B1[N1,K]^T, then, when B2 is not null, out2(bf16)[M,N2] = out1 . B2[N2,N1]^T
+ * in the same launch. Replaces the chunked np.matmul stages (ps/numerics.py:244-255) for short miss suffixes.
+ * Requires 1 <= M <= 256, N % 256 == 0, K % 64 == 0 (N1 % 64 == 0 for the second phase). */
+int po_op_stream_gemm(const void* A, int64_t lda, const void* B1, int64_t ldb1, void* out1, int64_t ldo1, int32_t M,
+                      int32_t N1, int32_t K, const void* B2, int64_t ldb2, void* out2, int64_t ldo2, int32_t N2,
+                      void* stream);
+
 /* Per-row dynamic E4M3 quantisation of a bf16 [rows, cols] matrix (activations before an FP8 GEMM, or weight
  * rows = output channels): scale[r] = amax_r / 448, q[r,c] = e4m3_satfinite_rn(x[r,c] * (448 / amax_r)).
  * cols % 16 == 0, ldx % 8 == 0, ldq % 16 == 0 (elements / bytes). */

@@ -61,6 +61,7 @@ SIGNATURES = {
     "po_op_gemm_fp8": (_I32, [_VP, _I64, _VP, _VP, _I64, _VP, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP, _I32,
                               _I32, _VP]),
     "po_op_quantize_e4m3": (_I32, [_VP, _I64, _I32, _I32, _VP, _I64, _VP, _VP]),
+    "po_op_stream_gemm": (_I32, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _I64, _VP, _I64, _I32, _VP]),
 }
 
 

@@ -707,12 +707,14 @@ bool pool_direct_enabled() {
 enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
               KC_STREAM, KC_COUNT };
 
-// PO_STREAM=0 runs prefix hits through the per-GEMM launches instead of the streaming kernel (A/B runs)
+// PO_STREAM=1 runs prefix hits' layer GEMMs through the persistent streaming kernel (stream.cu). Off by default:
+// its mainloop streams weights faster than the per-GEMM launches, but the in-kernel split-tile fix-up is
+// latency-bound with four epilogue warps per SM, so the forward is slower.
 bool stream_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* v = getenv("PO_STREAM");
-    on = (v && v[0] == '0') ? 0 : 1;
+    on = (v && v[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }

@@ -8,8 +8,26 @@
 //               split tiles; grid-barrier arrival after each phase
 #include "stream.cuh"
 #include "gemm_epi.cuh"
+#include <algorithm>
 
 namespace po {
+
+#ifdef STREAM_DBG_TRACE
+__device__ unsigned long long g_stream_trace[148 * 16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(i, cond) \
+  do {                 \
+    if (cond) g_stream_trace[blockIdx.x * 16 + (i)] = gtime(); \
+  } while (0)
+#else
+#define TRACE(i, cond) \
+  do {                 \
+  } while (0)
+#endif
 
 namespace {
 constexpr int BM = 128;                        // rows per CTA (pair tile: 256)
@@ -17,9 +35,12 @@ constexpr int BN = 256;                        // weight rows (output columns) p
 constexpr int BK = 64;
 constexpr int HALF = 128 * BK * 2;             // 16 KB: 128 rows x 64 bf16 (A half or B half per CTA)
 constexpr int STAGE = 2 * HALF;
-constexpr int STAGES = 6;
-constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+constexpr int STAGES = 5;
+constexpr int STG = 64 * 1024;                 // epilogue staging: partial dumps (4 warps x 2 x 4 KB), fix-up loads
+constexpr int RBUF = STG / 2;                  // one fix-up batch buffer (two, double buffered)
+constexpr int SMEM = STAGES * STAGE + STG + 1024 + 256 + 1024;
 constexpr int NT = 256;
+constexpr int FLAG_STRIDE = 32;                // one flag per 128-byte line: pollers of different flags never share one
 
 struct Geo {
   int nk, ntiles, spt, M, P;  // P: pairs with work (min(pairs, W): every one of them owns >= 1 k-block)
@@ -58,21 +79,90 @@ __device__ __forceinline__ Unit unit_at(const Geo& g, int pair, int kb) {
   return u;
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// spin until *p >= target, then an acquire fence. One thread per CTA polls the single counter line with growing
+// sleeps: 148 tight pollers saturate that line's L2 slice and stall every other access that hashes to it.
+__device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target) {
+  uint32_t ns = 64;
+  while (ld_relaxed_u64(p) < target) {
+    __nanosleep(ns);
+    ns = ns < 512 ? ns * 2 : 512;
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // generic-proxy writes of other CTAs (epilogue stores) -> this CTA's async-proxy reads (TMA), and the reverse
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Fused epilogue of one 4-column group of a fixed-up (summed) row: acc = columns col..col+3; part = the partner group
+// (gate -> up at col + 16; RoPE x1 -> x2 at col + 64); sc = the row's 1/rms (folded RMSNorm consumers); rv = the
+// residual row's values (EPI_RESID_F32). Same arithmetic order as epilogue_tile / splitk_reduce_quad.
+template <int EPI>
+__device__ __forceinline__ void quad_epi(const GemmArgs& a, int row, int col, float4 acc, float4 part, float sc,
+                                         float4 rv) {
+  if constexpr (EPI == EPI_BF16) {
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
+        make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    rv.x += acc.x; rv.y += acc.y; rv.z += acc.z; rv.w += acc.w;
+    *reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col) = rv;
+    if (a.xg_out) {
+      const float4 gm = *reinterpret_cast<const float4*>(a.g_next + col);
+      *reinterpret_cast<uint2*>(a.xg_out + (long long)row * a.ldxg + col) =
+          make_uint2(pack_bf16(rv.x * gm.x, rv.y * gm.y), pack_bf16(rv.z * gm.z, rv.w * gm.w));
+      float sq = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z + rv.w * rv.w;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if ((threadIdx.x & 31) == 0) a.ss_out[(long long)row * a.ss_nseg + col / 128] = sq;
+    }
+  } else if constexpr (EPI == EPI_SILU_MUL) {
+    const int oc = (col / 32) * 16 + (col % 32);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
+        make_uint2(pack_bf16(silu_f(sc * acc.x) * (sc * part.x), silu_f(sc * acc.y) * (sc * part.y)),
+                   pack_bf16(silu_f(sc * acc.z) * (sc * part.z), silu_f(sc * acc.w) * (sc * part.w)));
+  } else if constexpr (EPI == EPI_QKV_ROPE) {
+    const int head_col = col % 128;
+    acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+    if (a.bias) {
+      acc.x += a.bias[col]; acc.y += a.bias[col + 1]; acc.z += a.bias[col + 2]; acc.w += a.bias[col + 3];
+    }
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col;
+    if (col < a.rope_cols) {
+      float4 x2 = part;
+      x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
+      if (a.bias) {
+        x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
+      }
+      const float2* cs = a.rope + (long long)(a.pos_offset + row) * 64 + head_col;
+      const float2 c0 = cs[0], c1 = cs[1], c2 = cs[2], c3 = cs[3];
+      const uint2 lo = make_uint2(pack_bf16(acc.x * c0.x - x2.x * c0.y, acc.y * c1.x - x2.y * c1.y),
+                                  pack_bf16(acc.z * c2.x - x2.z * c2.y, acc.w * c3.x - x2.w * c3.y));
+      const uint2 hi = make_uint2(pack_bf16(x2.x * c0.x + acc.x * c0.y, x2.y * c1.x + acc.y * c1.y),
+                                  pack_bf16(x2.z * c2.x + acc.z * c2.y, x2.w * c3.x + acc.w * c3.y));
+      *reinterpret_cast<uint2*>(o) = lo;
+      *reinterpret_cast<uint2*>(o + 64) = hi;
+      if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) {
+        *reinterpret_cast<uint2*>(prow + col) = lo;
+        *reinterpret_cast<uint2*>(prow + col + 64) = hi;
+      }
+    } else {
+      const uint2 v = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+      *reinterpret_cast<uint2*>(o) = v;
+      if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) *reinterpret_cast<uint2*>(prow + col) = v;
+    }
+  }
+}
 
 }  // namespace
 
@@ -81,11 +171,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * HALF;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint8_t* stg = smem + STAGES * STAGE;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + STG);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* rbar = tempty_bar + 2;  // fix-up batch loads, one per buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  float* s_inv = reinterpret_cast<float*>(stg + STG + 256);  // 1/rms of the rows a fix-up reduces (<= 256)
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -105,6 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 2);
+      mbar_init(&rbar[s], 1);
     }
     fence_barrier_init();
   }
@@ -118,6 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
   // constant); everyone else waits now
   if (warp != 0) pdl_wait();
   pdl_trigger();
+  TRACE(0, threadIdx.x == 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -148,8 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
               if (f == 0) {
                 pdl_wait();
               } else {
-                const unsigned long long target = A.bar_base + (unsigned long long)f * gridDim.x;
-                while (ld_acquire_u64(A.bar) < target) __nanosleep(64);
+                wait_counter(A.bar, A.bar_base + (unsigned long long)f * gridDim.x);
               }
               fence_proxy_async_global();
               open = true;
@@ -161,6 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
           }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        TRACE(1, f == 0);
         if (f == 0 && !open) pdl_wait();
       }
     }
@@ -204,6 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
     const int row = rank * BM + wq * 32 + lane;  // accumulator row of this thread (single 256-row m tile)
     int it = 0;
+    uint32_t rb = 0;  // fix-up batches so far: buffer rb & 1, mbarrier parity (rb >> 1) & 1
     for (int f = 0; f < A.nph; ++f) {
       const StreamPhase& F = A.ph[f];
       const Geo g = geo_of(F, P);
@@ -218,31 +314,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
         const uint32_t acc_ph = (it >> 1) & 1;
         mbar_wait(&tfull_bar[acc], acc_ph);
         tc_fence_after();
+        TRACE(2, f == 0 && et == 0 && kb == u.kb1 - u.kb0 + range_lo(g, pair));
+        TRACE(3, f == 0 && et == 0);
         const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
         if (u.nseg > 1) {
           // a tile cut across pairs: dump this segment's fp32 partial and raise its flag; the segments' owners
           // reduce the tile together once all are in (below)
+          // Layout of a partial slot: [8 column chunks][M rows][32 fp32], 128-byte rows with float4 q stored at
+          // q ^ (row & 7). Each warp stages its 32 rows x 32 columns in shared memory and one lane writes the 4 KB
+          // block with a bulk copy (full-line writes instead of 1 KB-strided per-thread stores).
           const long long slot = (long long)u.tile * g.spt + u.seg;
-          float* dst = A.ws + slot * slot_elems + (long long)row * BN;
+          const int rowbase = rank * BM + wq * 32;
+          const int valid = min(max(g.M - rowbase, 0), 32);
+          float* dst0 = A.ws + slot * slot_elems + (long long)rowbase * 32;
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = 0; c < 8; ++c) {
             uint32_t r[32];
-            tmem_ld32(taddr + c, r);
+            tmem_ld32(taddr + c * 32, r);
+            uint8_t* wb = stg + (wq * 2 + (c & 1)) * 4096;
+            if (lane == 0) bulk_wait_read<1>();  // the copy that last read this buffer (chunk c - 2) is done
+            __syncwarp();
             tmem_ld_wait();
-            if (row < g.M) {
-              float4* d4 = reinterpret_cast<float4*>(dst + c);
 #pragma unroll
-              for (int q = 0; q < 8; ++q)
-                d4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(wb + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                              __uint_as_float(r[4 * q + 3]));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && valid > 0) {
+              bulk_s2g(dst0 + (long long)c * g.M * 32, wb, valid * 128);
+              bulk_commit();
             }
+          }
+          if (lane == 0) {
+            bulk_wait_all();
+            fence_proxy_async_global();
           }
           tc_fence_before();
           named_bar_sync(1, 128);
           if (et == 0) {
             mbar_arrive_cluster(tempty0 + acc * 8);
             __threadfence();
-            st_release_u32(A.flags + slot * 2 + rank, tag);
+            st_release_u32(A.flags + (slot * 2 + rank) * FLAG_STRIDE, tag);
           }
           split_tiles[nsplit++] = u.tile;
         } else {
@@ -258,6 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
           if (et == 0) mbar_arrive_cluster(tempty0 + acc * 8);
         }
       }
+      TRACE(4, f == 0 && et == 0);
       // cooperative fix-up of the split tiles this pair holds a segment of (at most two: its first and last unit):
       // the tile's 2 x nseg CTAs each sum every segment for an interleaved share of its rows, in segment order
       for (int i = 0; i < nsplit; ++i) {
@@ -265,31 +380,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) stream_kernel
         const int q0 = stream_owner(g.W, g.P, t * g.nk);
         const int nseg = stream_owner(g.W, g.P, t * g.nk + g.nk - 1) - q0 + 1;
         const long long slot0 = (long long)t * g.spt;
-        if (et == 0) {
-          const int ranks = g.M > BM ? 2 : 1;  // a CTA with no rows below M dumps nothing but still flags
-          for (int j = 0; j < nseg; ++j)
-            for (int r = 0; r < ranks; ++r)
-              while (ld_acquire_u32(A.flags + (slot0 + j) * 2 + r) != tag) __nanosleep(32);
-        }
-        named_bar_sync(2, 128);
+        // this CTA's contiguous share of the tile's rows, reduced in batches of B rows (all segments of a batch
+        // fit one RBUF buffer and are fetched by bulk copies, double buffered)
         const int workers = 2 * nseg, worker = 2 * (pair - q0) + rank;
-        const int sub = et >> 6, c = (et & 63) * 4;  // two rows per pass; each warp one 128-column segment
-        const float* base = A.ws + slot0 * slot_elems + c;
-        for (int rr = 2 * worker + sub; rr < g.M; rr += 2 * workers) {
-          const float* p = base + (long long)rr * BN;
-          switch (F.epi) {
-            case EPI_RESID_F32: splitk_reduce_quad<EPI_RESID_F32>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
-            case EPI_SILU_MUL: splitk_reduce_quad<EPI_SILU_MUL>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
-            case EPI_QKV_ROPE: splitk_reduce_quad<EPI_QKV_ROPE>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
-            default: splitk_reduce_quad<EPI_BF16>(F.g, rr, t * BN + c, p, slot_elems, nseg); break;
+        const int r0 = (int)((long long)worker * g.M / workers), r1 = (int)((long long)(worker + 1) * g.M / workers);
+        const int B = min(16, RBUF / (nseg * 1024));
+        if (et < 32) {
+          // every segment's flag (both CTA halves when rows reach the second), polled in parallel by one warp, then
+          // one acquire fence
+          const int nfl = nseg * (g.M > BM ? 2 : 1);
+          const int stride = g.M > BM ? 1 : 2;
+          uint32_t ns = 64;
+          for (;;) {
+            bool ok = true;
+            for (int k = lane; k < nfl; k += 32)
+              ok &= ld_relaxed_u32(A.flags + (slot0 * 2 + k * stride) * FLAG_STRIDE) == tag;
+            if (__all_sync(0xffffffffu, ok)) break;
+            __nanosleep(ns);
+            ns = ns < 256 ? ns * 2 : 256;
           }
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
+        // the folded-norm consumers scale rows by 1/rms: one load chain per row, up front
+        if (F.epi == EPI_SILU_MUL || F.epi == EPI_QKV_ROPE)
+          for (int rr = r0 + et; rr < r1; rr += 128) s_inv[rr - r0] = F.g.ss_in ? row_inv_rms(F.g, rr) : 1.0f;
+        named_bar_sync(2, 128);
+        TRACE(5, f == 0 && et == 0 && i == 0);
+        TRACE(14, f == 0 && et == 0 && i == 1);
+        const float* seg0 = A.ws + slot0 * slot_elems;
+        // one batch = nseg x 8 bulk copies (segment j, column chunk c), spread over the lanes of the first warp
+        auto issue = [&](int b0, int buf) {
+          const int nb = min(B, r1 - b0);
+          if (lane == 0) mbar_arrive_expect_tx(&rbar[buf], nseg * 8 * nb * 128);
+          __syncwarp();
+          uint8_t* dstb = stg + buf * RBUF;
+          for (int k = lane; k < nseg * 8; k += 32) {
+            const int j = k >> 3, c = k & 7;
+            bulk_g2s(dstb + k * B * 128, seg0 + j * slot_elems + ((long long)c * g.M + b0) * 32, nb * 128, &rbar[buf]);
+          }
+        };
+        if (r0 < r1 && et < 32) issue(r0, rb & 1);
+        for (int b0 = r0; b0 < r1; b0 += B, ++rb) {
+          const int buf = rb & 1;
+          if (b0 + B < r1 && et < 32) issue(b0 + B, buf ^ 1);
+          const int nb = min(B, r1 - b0);
+          // items: (row, quad) with each warp on one 128-column half of a row (RESID's sum of squares)
+          const int q = (et & 63);
+          const int c4 = q * 4;
+          float4 rv[8];
+          if (F.epi == EPI_RESID_F32) {  // residual rows in flight before the partials land
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int rl = (et >> 6) + 2 * k;
+              if (rl < nb)
+                rv[k] = __ldcg(reinterpret_cast<const float4*>(F.g.resid + (long long)(b0 + rl) * F.g.ldr + t * BN + c4));
+            }
+          }
+          mbar_wait(&rbar[buf], (rb >> 1) & 1);
+          TRACE(8 + (b0 - r0) / B, f == 0 && et == 0 && i == 0 && (b0 - r0) / B < 5);
+          const uint8_t* rbuf = stg + buf * RBUF;
+          auto sum_quad = [&](int rl, int qd) {
+            const int row_g = b0 + rl;
+            const uint8_t* pq = rbuf + ((qd >> 3) * B + rl) * 128 + (((qd & 7) ^ (row_g & 7)) << 4);
+            float4 acc = *reinterpret_cast<const float4*>(pq);
+            for (int j = 1; j < nseg; ++j) {
+              const float4 v = *reinterpret_cast<const float4*>(pq + j * 8 * B * 128);
+              acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+            return acc;
+          };
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int rl = (et >> 6) + 2 * k;
+            if (rl >= nb) break;  // warp-uniform
+            const int row_g = b0 + rl;
+            const int col = t * BN + c4;
+            switch (F.epi) {
+              case EPI_RESID_F32: quad_epi<EPI_RESID_F32>(F.g, row_g, col, sum_quad(rl, q), float4{}, 1.f, rv[k]); break;
+              case EPI_SILU_MUL:
+                if ((q & 7) < 4)
+                  quad_epi<EPI_SILU_MUL>(F.g, row_g, col, sum_quad(rl, q), sum_quad(rl, q + 4), s_inv[row_g - r0], rv[k]);
+                break;
+              case EPI_QKV_ROPE: {
+                const bool lo_half = (q & 31) < 16;
+                const bool rot = col < F.g.rope_cols;
+                if (!rot || lo_half)
+                  quad_epi<EPI_QKV_ROPE>(F.g, row_g, col, sum_quad(rl, q), rot ? sum_quad(rl, q + 16) : float4{},
+                                         s_inv[row_g - r0], rv[k]);
+                break;
+              }
+              default: quad_epi<EPI_BF16>(F.g, row_g, col, sum_quad(rl, q), float4{}, 1.f, rv[k]); break;
+            }
+          }
+          named_bar_sync(2, 128);  // every thread is done with this buffer before it is refilled
+        }
+        TRACE(13 + 2 * i, f == 0 && et == 0 && i < 2);
       }
+      TRACE(6, f == 0 && et == 0);
       // this CTA's outputs of phase f are stored: arrive on the grid barrier
       named_bar_sync(1, 128);
       if (et == 0) {
+        // one counter serves every phase: a CTA with no work in phase f must not arrive for it before the barrier of
+        // phase f - 1 is complete, or its arrival would be counted toward f - 1
+        if (f > 0) {
+          wait_counter(A.bar, A.bar_base + (unsigned long long)f * gridDim.x);
+        }
         fence_proxy_async_global();
         __threadfence();
+        TRACE(7, f == 0);
         atomicAdd(A.bar, 1ull);
       }
     }
@@ -321,7 +519,7 @@ static int slots_per_tile(int N, int K) {
 }
 
 size_t stream_ws_bytes(int M, int N, int K) { return (size_t)(N / BN) * slots_per_tile(N, K) * M * BN * sizeof(float); }
-size_t stream_flag_count(int N, int K) { return (size_t)(N / BN) * slots_per_tile(N, K) * 2; }
+size_t stream_flag_count(int N, int K) { return (size_t)(N / BN) * slots_per_tile(N, K) * 2 * FLAG_STRIDE; }
 
 int stream_launch(StreamArgs& a, cudaStream_t stream) {
   if (a.nph <= 0 || a.nph > STREAM_MAX_PHASES) return -3;
@@ -330,6 +528,7 @@ int stream_launch(StreamArgs& a, cudaStream_t stream) {
     const GemmArgs& g = p.g;
     if (g.M <= 0 || g.M > 2 * BM || g.N % BN || g.K % BK) return -3;
     p.slots_per_tile = slots_per_tile(g.N, g.K);
+    if (p.slots_per_tile * 1024 > RBUF) return -3;  // one row of every segment must fit a fix-up buffer
     if (stream_ws_bytes(g.M, g.N, g.K) > a.ws_bytes || stream_flag_count(g.N, g.K) > a.n_flags) return -3;
   }
   ensure_smem_attr<stream_kernel>(SMEM);
@@ -338,3 +537,78 @@ int stream_launch(StreamArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace po
+
+// ------------------------------------------------------------------ C-ABI op (kernel-level parity tests, A/B timing)
+#include "../../include/prefillonly.h"
+namespace po {
+int set_error(int code, const char* fmt, ...);
+void keep_pool_memory();
+}  // namespace po
+
+extern "C" int po_op_stream_gemm(const void* A, int64_t lda, const void* B1, int64_t ldb1, void* out1, int64_t ldo1,
+                                 int32_t M, int32_t N1, int32_t K, const void* B2, int64_t ldb2, void* out2,
+                                 int64_t ldo2, int32_t N2, void* stream) {
+  using namespace po;
+  if (!A || !B1 || !out1 || (B2 && !out2)) return set_error(PO_ERR_ARG, "po_op_stream_gemm: null pointer");
+  if (M < 1 || M > 256 || N1 <= 0 || N1 % 256 || K <= 0 || K % 64 || (B2 && (N2 <= 0 || N2 % 256)))
+    return set_error(PO_ERR_ARG, "po_op_stream_gemm: need 1 <= M <= 256, N %% 256 == 0, K %% 64 == 0");
+  StreamArgs a{};
+  a.nph = B2 ? 2 : 1;
+  auto phase = [&](StreamPhase& p, const void* x, long long ldx, int k, const void* w, long long ldw, int n, void* o,
+                   long long ldo) {
+    p.g.M = M; p.g.N = n; p.g.K = k; p.g.out = o; p.g.ldo = ldo;
+    p.epi = EPI_BF16;
+    return make_tmap_a(&p.a, x, ldx, M, k) || make_tmap_a(&p.b, w, ldw, n, k);
+  };
+  if (phase(a.ph[0], A, lda, K, B1, ldb1, N1, out1, ldo1) ||
+      (B2 && phase(a.ph[1], out1, ldo1, N1, B2, ldb2, N2, out2, ldo2)))
+    return set_error(PO_ERR_ARG, "po_op_stream_gemm: tensor-map encode failed (alignment?)");
+  // the op keeps one workspace per device, a monotonic barrier counter and a fresh tag per call, like an engine
+  struct Ws {
+    void* buf = nullptr;
+    size_t ws = 0, nf = 0;
+    unsigned long long base = 0;
+    uint32_t tag = 0;
+  };
+  static Ws per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Ws& w = per_dev[dev & 63];
+  const size_t need_ws = std::max(stream_ws_bytes(M, N1, K), B2 ? stream_ws_bytes(M, N2, N1) : 0);
+  const size_t need_nf = std::max(stream_flag_count(N1, K), B2 ? stream_flag_count(N2, N1) : 0);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!w.buf || need_ws > w.ws || need_nf > w.nf) {
+    if (w.buf) {
+      cudaDeviceSynchronize();
+      cudaFree(w.buf);
+    }
+    w.ws = std::max(need_ws, w.ws);
+    w.nf = std::max(need_nf, w.nf);
+    const size_t fl_off = (w.ws + 255) / 256 * 256, bar_off = fl_off + (w.nf * 4 + 255) / 256 * 256;
+    if (cudaMalloc(&w.buf, bar_off + 8) != cudaSuccess || cudaMemset(w.buf, 0, bar_off + 8) != cudaSuccess) {
+      w.buf = nullptr;
+      return set_error(PO_ERR_CUDA, "po_op_stream_gemm: workspace allocation failed");
+    }
+    w.base = 0;
+    w.tag = 0;
+  }
+  const size_t fl_off = (w.ws + 255) / 256 * 256, bar_off = fl_off + (w.nf * 4 + 255) / 256 * 256;
+  a.ws = static_cast<float*>(w.buf);
+  a.ws_bytes = w.ws;
+  a.flags = reinterpret_cast<uint32_t*>(static_cast<char*>(w.buf) + fl_off);
+  a.n_flags = w.nf;
+  a.bar = reinterpret_cast<unsigned long long*>(static_cast<char*>(w.buf) + bar_off);
+  a.bar_base = w.base;
+  a.tag = ++w.tag;
+  const int rc = stream_launch(a, st);
+  if (!rc) w.base += (unsigned long long)a.nph * 2 * stream_pairs();
+  if (rc) return set_error(PO_ERR_CUDA, "po_op_stream_gemm: launch failed (%d): %s", rc,
+                           cudaGetErrorString(cudaGetLastError()));
+  return PO_OK;
+}
+
+#ifdef STREAM_DBG_TRACE
+extern "C" int po_debug_stream_trace(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, po::g_stream_trace, sizeof(unsigned long long) * 148 * 16) == cudaSuccess ? 0 : -1;
+}
+#endif
