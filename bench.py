@@ -21,8 +21,8 @@ request with a Yes/No allowed list, cold prefix cache. One STEP = one request th
           latency meets the SLO. The event loop is the reference's (serving.simulate, virtual clock); every
           request of the saturation run is executed for real on the GPU in serving order and its measured
           device time reused by the rate sweep (serving.ReplayServiceFn).
-  cpu_baseline  the CPU port of the reference path (oracle/llama_ref.py, numpy f64) timed on this host on a
-          bounded sample (one Llama-8B layer at 1,024 tokens), extrapolated by the FLOP formula.
+  cpu_baseline  the reference's own layer forward (stock prefillsim block_forward_hybrid from baseline/_ref, numpy
+          f64) timed on this host at 1,024 / 2,048 / 4,096 tokens and extrapolated to the 20k request by a fit.
 """
 
 from __future__ import annotations
@@ -120,8 +120,68 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------------- CPU arm
+REF_SIZES = (1024, 2048, 4096)
+
+
+def _stock_numerics():
+    """The reference's own layer forward: prefillsim.numerics from the offline install in baseline/_ref (the stock
+    package built from /root/reference, imported unmodified); None when it is not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "prefillsim" / "numerics.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    from prefillsim import numerics
+
+    return numerics
+
+
+class StockReference:
+    """Times the stock reference forward `block_forward_hybrid` (ps/numerics.py:215-275: float64 numpy, chunked
+    linear stages, full-length attention) at the Llama-3.1-8B layer shape (hidden 4096, intermediate 14336, chunk
+    8192, preallocated in-place outputs) and extrapolates a 20k-token, 32-layer request from a least-squares fit
+    t(n) = a*n + b*n^2 over the measured sizes (linear stages ~ n, the reference's full n x n attention ~ n^2)."""
+
+    def __init__(self, numerics, seed: int = 0):
+        from paper_2505_07203_b200.config import LLAMA_3_1_8B as M
+
+        self.nm = numerics
+        self.M = M
+        self.params = numerics.ToyBlockParams.random(seed, M.hidden, M.intermediate)
+        self.samples: list[tuple[int, float]] = []
+
+    def step(self, n: int, record: bool = True) -> float:
+        x = self.nm.random_input(n, n, self.M.hidden)
+        t0 = time.perf_counter()
+        self.nm.block_forward_hybrid(self.params, x, 8192, self.nm.ScratchTracker(), prealloc=True, inplace=True)
+        dt = time.perf_counter() - t0
+        if record:
+            self.samples.append((n, dt))
+        return dt
+
+    def fit(self) -> tuple[float, float]:
+        ns = np.array([n for n, _ in self.samples], dtype=np.float64)
+        ts = np.array([t for _, t in self.samples], dtype=np.float64)
+        (a, b), *_ = np.linalg.lstsq(np.stack([ns, ns * ns], axis=1), ts, rcond=None)
+        return float(a), float(b)
+
+    def request_seconds(self, n_tokens: int) -> float:
+        a, b = self.fit()
+        return self.M.num_layers * (a * n_tokens + b * n_tokens * n_tokens)
+
+    def summary(self, n_tokens: int) -> dict:
+        a, b = self.fit()
+        per = {}
+        for n, t in self.samples:
+            per.setdefault(n, []).append(t)
+        return {"layer_seconds": {str(n): statistics.median(v) for n, v in sorted(per.items())},
+                "fit_s": {"a_per_token": a, "b_per_token2": b},
+                "request_seconds_extrapolated": self.request_seconds(n_tokens)}
+
+
 def cpu_layer_sample(n: int = 1024, seed: int = 0):
-    """Time the CPU port of the reference path (oracle/llama_ref.py, f64 numpy) on one Llama-8B layer."""
+    """The CPU port of the path (oracle/llama_ref.py, f64 numpy) on one Llama-8B layer (used when the stock
+    reference is not installed, and for the tiny configs[0] request)."""
     from oracle import llama_ref
     from paper_2505_07203_b200.config import LLAMA_3_1_8B as M
 
@@ -148,6 +208,19 @@ def cpu_layer_sample(n: int = 1024, seed: int = 0):
     return run, flops
 
 
+def tiny_request_seconds() -> float:
+    """configs[0]: the tiny 2-layer model's 2,048-token Yes/No request through the CPU oracle (port), seconds."""
+    from oracle import llama_ref
+    from paper_2505_07203_b200.config import TINY
+
+    cfg = llama_ref.Cfg.from_model(TINY)
+    w = llama_ref.make_weights(cfg, 42)
+    toks = np.random.default_rng([0, 0, 0]).integers(0, 2 ** 32, size=2048, dtype=np.uint32)
+    t0 = time.perf_counter()
+    llama_ref.llama_forward(cfg, w, toks, ALLOWED)
+    return time.perf_counter() - t0
+
+
 def blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
@@ -157,6 +230,16 @@ def blas_threads() -> int:
         return os.cpu_count() or 1
 
 
+def blas_name() -> str:
+    try:
+        from threadpoolctl import threadpool_info
+
+        infos = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        return f"{infos[0].get('internal_api')} {infos[0].get('version')}" if infos else "unknown"
+    except Exception:
+        return "unknown"
+
+
 def cpu_tokens_per_s(seconds: float, sample_flops: float, n_tokens: int) -> float:
     from paper_2505_07203_b200.config import LLAMA_3_1_8B as M
 
@@ -164,8 +247,45 @@ def cpu_tokens_per_s(seconds: float, sample_flops: float, n_tokens: int) -> floa
     return n_tokens / (M.request_flops(n_tokens) / rate)
 
 
+def cpu_baseline_sample(n_tokens: int) -> dict:
+    """Bounded CPU sample for the GPU arm's `cpu_baseline` (rank 0, N = 1): the stock reference forward at
+    REF_SIZES tokens (one layer each, ~10-20 s of CPU work), extrapolated to the request; the port if the
+    reference is not installed."""
+    nm = _stock_numerics()
+    if nm is not None:
+        ref = StockReference(nm)
+        ref.step(512, record=False)  # warm the BLAS threads
+        for n in REF_SIZES:
+            ref.step(n)
+        sec = ref.request_seconds(n_tokens)
+        sm = ref.summary(n_tokens)
+        return {"value": n_tokens / sec, "unit": UNIT, "cores": blas_threads(), "kind": "reference",
+                "sample": f"stock prefillsim.numerics.block_forward_hybrid (baseline/_ref) at hidden 4096 / "
+                          f"intermediate 14336, one layer at each of {list(REF_SIZES)} tokens "
+                          f"({', '.join(f'{float(v):.2f} s' for v in sm['layer_seconds'].values())}), fit "
+                          f"t = a n + b n^2, extrapolated to 32 layers x {n_tokens} tokens",
+                "fit": sm, "blas": blas_name(), "host_cpus": os.cpu_count()}
+    run, flops = cpu_layer_sample()
+    run()
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 10.0 or reps < 2:
+        run()
+        reps += 1
+    sec = (time.perf_counter() - t0) / reps
+    return {"value": cpu_tokens_per_s(sec, flops, n_tokens), "unit": UNIT, "cores": blas_threads(), "kind": "port",
+            "sample": f"{reps} x one Llama-3.1-8B layer at 1,024 tokens (float64 numpy CPU port of the reference "
+                      f"path, oracle/llama_ref.py), {sec:.2f} s each, extrapolated by the FLOP formula to 32 layers "
+                      f"x {n_tokens} tokens", "host_cpus": os.cpu_count()}
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the reference path's CPU implementation (the oracle port) on the host cores."""
+    """--impl reference: the reference's own CPU implementation of the path on the host cores.
+
+    Each step runs the stock `prefillsim.numerics.block_forward_hybrid` (installed unmodified into baseline/_ref)
+    for one Llama-8B-shaped layer at 1,024 / 2,048 / 4,096 tokens in turn; the value is the 20k-token, 32-layer
+    request extrapolated from the fit over all timed steps. The CPU port (oracle/llama_ref.py) is the fallback
+    when the install is missing."""
     if rank != 0:
         return
     # every host thread for the BLAS (torchrun sets OMP_NUM_THREADS=1 for its workers; the other ranks idle here)
@@ -175,31 +295,58 @@ def run_reference(args, world, rank):
         limits = threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
     except Exception:
         limits = None
-    run, flops = cpu_layer_sample()
-    for _ in range(args.warmup):
-        run()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    t = sum(times)
-    value = cpu_tokens_per_s(t / args.steps, flops, args.n_tokens)
+    nm = _stock_numerics()
+    extra = {}
+    if nm is not None:
+        ref = StockReference(nm)
+        for i in range(args.warmup):
+            ref.step(REF_SIZES[0], record=False)
+        t_all = 0.0
+        for i in range(args.steps):
+            t_all += ref.step(REF_SIZES[i % len(REF_SIZES)])
+        if args.steps < 2:  # a fit needs two sizes
+            t_all += ref.step(REF_SIZES[1])
+        request_s = ref.request_seconds(args.n_tokens)
+        value = args.n_tokens / request_s
+        kind = "reference"
+        sample = (f"stock prefillsim.numerics.block_forward_hybrid (baseline/_ref, unmodified) at hidden 4096 / "
+                  f"intermediate 14336, one layer per step cycling {list(REF_SIZES)} tokens, fit t = a n + b n^2, "
+                  f"extrapolated to 32 layers x {args.n_tokens} tokens ({request_s:.0f} s per request)")
+        extra = {"fit": ref.summary(args.n_tokens)}
+        ms_per_step = 1e3 * t_all / max(1, len(ref.samples))
+    else:
+        run, flops = cpu_layer_sample()
+        for _ in range(args.warmup):
+            run()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t0)
+        value = cpu_tokens_per_s(sum(times) / args.steps, flops, args.n_tokens)
+        kind = "port"
+        sample = (f"one Llama-3.1-8B layer at 1,024 tokens in float64 numpy per step (oracle/llama_ref.py), "
+                  f"extrapolated by the FLOP formula to 32 layers x {args.n_tokens} tokens")
+        ms_per_step = 1e3 * sum(times) / args.steps
+    try:
+        extra["tiny_config0_request_s"] = tiny_request_seconds()
+    except Exception as exc:  # noqa: BLE001 - informational only
+        extra["tiny_config0_request_s"] = f"failed: {exc}"
     cores = blas_threads()
     if limits is not None:
         limits.restore_original_limits()
-    sample = (f"one Llama-3.1-8B layer (RMSNorm, QKV+RoPE, causal GQA attention, O, SiLU MLP) at 1,024 tokens in "
-              f"float64 numpy per step, extrapolated by the FLOP formula to 32 layers x {args.n_tokens} tokens")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (random weights, random activations)",
         "config": workload_config(args, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "blas": blas_name(), "host_cpus": os.cpu_count(), **extra},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "the reference (arxiv 2505.07203 prefillsim) is a pure-Python simulator with no engine; its "
-                "layer-forward semantics (ps/numerics.py) are timed through the CPU port oracle/llama_ref.py",
+        "note": "the reference (arxiv 2505.07203 prefillsim) models serving analytically; its own implementation of "
+                "the layer forward (ps/numerics.py block_forward_hybrid, single-head toy block, float64) is what "
+                "runs here. tiny_config0_request_s: BASELINE configs[0] through the CPU port oracle",
     }), flush=True)
 
 
@@ -399,22 +546,10 @@ def main():
     # ---------------- prefix-hit forward (the serving path after a cache hit): an HBM-bound weight stream
     hit = prefix_hit_roofline(eng, M, n, peaks) if rank == 0 and not args.no_qps else None
 
-    # ---------------- CPU baseline (rank 0, N = 1 only)
+    # ---------------- CPU baseline (rank 0, N = 1 only): the stock reference forward on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        run, flops = cpu_layer_sample()
-        run()
-        t0 = time.perf_counter()
-        reps = 0
-        while time.perf_counter() - t0 < 10.0 or reps < 2:
-            run()
-            reps += 1
-        sec = (time.perf_counter() - t0) / reps
-        cpu = {"value": cpu_tokens_per_s(sec, flops, n), "unit": UNIT, "cores": blas_threads(), "kind": "port",
-               "sample": f"{reps} x one Llama-3.1-8B layer at 1,024 tokens (float64 numpy CPU port of the "
-                         f"reference path, oracle/llama_ref.py), {sec:.2f} s each, extrapolated by the FLOP "
-                         f"formula to 32 layers x {n} tokens",
-               "host_cpus": os.cpu_count()}
+        cpu = cpu_baseline_sample(n)
 
     if rank == 0:
         line = {
