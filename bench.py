@@ -18,9 +18,10 @@ request with a Yes/No allowed list, cold prefix cache. One STEP = one request th
           `value` region because they break the PDL overlap); `roofline` is the class with the largest share.
   qps_at_slo  post-recommendation 20k workload (40 users x 50 requests, shared profiles) under Poisson
           arrivals, calibrated SRJF + prefix pool, sticky routing over N GPUs: largest rate whose p99
-          latency meets the SLO. The event loop is the reference's (serving.simulate, virtual clock); every
-          request of the saturation run is executed for real on the GPU in serving order and its measured
-          device time reused by the rate sweep (serving.ReplayServiceFn).
+          latency meets the SLO. Each rank serves its own shard on its own GPU (records gathered for the
+          global p99). The event loop is the reference's (serving.simulate, virtual clock); every request of
+          the saturation run is executed for real in serving order and its measured device time reused by
+          the rate sweep (serving.ReplayServiceFn); a wall-clock Server run at the knee rate is reported beside.
   cpu_baseline  the reference's own layer forward (stock prefillsim block_forward_hybrid from baseline/_ref, numpy
           f64) timed on this host at 1,024 / 2,048 / 4,096 tokens and extrapolated to the 20k request by a fit.
 """
@@ -542,6 +543,7 @@ def main():
     qps = None
     if not args.no_qps:
         qps = qps_at_slo(eng, M, world, rank, args.slo, dist if world > 1 else None)
+        barrier()
 
     # ---------------- prefix-hit forward (the serving path after a cache hit): an HBM-bound weight stream
     hit = prefix_hit_roofline(eng, M, n, peaks) if rank == 0 and not args.no_qps else None
@@ -592,58 +594,99 @@ def prefix_hit_roofline(eng, M, n, peaks):
 
 
 def qps_at_slo(eng, M, world, rank, slo, dist):
-    """Calibrated-SRJF serving of the post-recommendation 20k workload over `world` GPU replicas.
+    """Calibrated-SRJF serving of the post-recommendation 20k workload, request-level DP over `world` GPUs.
 
-    Virtual-clock event loop with the reference's semantics (serving.simulate); every request of the saturation
-    run executes for real on this GPU in serving order (ReplayServiceFn) and the rate sweep reuses those device
-    times. Rank 0 runs the loop for all replicas (identical GPUs, sticky user routing).
+    Every rank serves its own shard of the trace (sticky user routing, `serving.shard_trace`, ps/sim.py:52-66) on its
+    own engine and prefix pool; the per-rank records are gathered (`merge_records`) for the global p99, and every
+    rank takes the same decisions from the merged report. Virtual-clock event loop with the reference's semantics
+    (serving.simulate, ps/sim.py:211-269): each rank's requests of the saturation run execute for real on that
+    rank's GPU in serving order (ReplayServiceFn) and the rate sweep reuses those device times. At the knee rate a
+    wall-clock run (serving.Server + replay: real arrivals in real time, host-side hashing, scheduling and ctypes
+    inside the latency) is reported beside it.
     """
+    from paper_2505_07203_b200 import jct as J
     from paper_2505_07203_b200 import workload as wl
-    from paper_2505_07203_b200.scheduling import Policy
-    from paper_2505_07203_b200.serving import ReplayServiceFn, qps_at_slo as pick, refine_qps, simulate, sweep_rates
+    from paper_2505_07203_b200.scheduling import SCORING_PROFILE, Policy
+    from paper_2505_07203_b200.serving import (ReplayServiceFn, Server, merge_records, qps_at_slo as pick,
+                                               refine_qps, replay, shard_trace, simulate, sweep_rates)
 
-    if rank != 0:
-        return None
     trace = wl.gen_post_recommendation(0, wl.POSTREC_20K)
     capacity = min(eng.capacity_tokens, 16 * eng.pool_blocks)
     t0 = time.perf_counter()
+
+    def merged(local):
+        if world == 1:
+            return local
+        allr = [None] * world
+        dist.all_gather_object(allr, list(local.records))
+        return merge_records(allr, world)
+
     # the paper's calibration (PAPER.md:634-657, 942): JCT profile fitted on this GPU's measured latencies
     # (ps/jct.py:100-128 with the real engine as latency_fn), seconds-valued scores, lambda = 500
-    from paper_2505_07203_b200 import jct as J
-    from paper_2505_07203_b200.scheduling import SCORING_PROFILE
-
     jprof = J.fit(J.profile_engine(eng, max_input=24_000, step=4000))
     svc = ReplayServiceFn(eng, ALLOWED)
-    run = lambda tr, pol=None: simulate(tr, world, pol or Policy.srjf_calibrated(), capacity, svc)  # noqa: E731
-    sat = run(wl.zero_arrivals(trace)).throughput  # every request runs for real here, in serving order
+
+    def run(tr, pol=None, jp=None):
+        mine = shard_trace(tr, rank, world)
+        return merged(simulate(mine, 1, pol or Policy.srjf_calibrated(), capacity, svc, jct_profile=jp))
+
+    sat_rep = run(wl.zero_arrivals(trace))  # every request runs for real here, in its rank's serving order
+    sat = sat_rep.throughput
     svc.recording = False
     rates = [sat * m for m in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0)]
-    res = sweep_rates(trace, rates, seed=0, run=run)
-    fifo = sweep_rates(trace, rates, seed=0, run=lambda tr: run(tr, Policy.fifo()))
+    sweep = lambda pol, jp=None: (lambda tr: run(tr, pol, jp))  # noqa: E731
+    res = sweep_rates(trace, rates, seed=0, run=sweep(None))
+    fifo = sweep_rates(trace, rates, seed=0, run=sweep(Policy.fifo()))
     # resolve the knee: bisect between the last rate meeting the SLO and the first one above it that misses
-    res = refine_qps(res, slo, lambda q: sweep_rates(trace, [q], seed=0, run=run)[0][1])
-    fifo = refine_qps(fifo, slo, lambda q: sweep_rates(trace, [q], seed=0, run=lambda tr: run(tr, Policy.fifo()))[0][1])
-    # the paper's default fairness weight (PAPER.md:942, lambda = 500) beside the reference's (0.5, same units: miss
-    # tokens per second of queueing)
-    pol500 = Policy.srjf_calibrated(lam=500.0)
-    run500 = lambda tr: run(tr, pol500)  # noqa: E731
-    res500 = refine_qps(sweep_rates(trace, rates, seed=0, run=run500), slo,
-                        lambda q: sweep_rates(trace, [q], seed=0, run=run500)[0][1])
+    res = refine_qps(res, slo, lambda q: sweep_rates(trace, [q], seed=0, run=sweep(None))[0][1])
+    fifo = refine_qps(fifo, slo, lambda q: sweep_rates(trace, [q], seed=0, run=sweep(Policy.fifo()))[0][1])
     polp = Policy.srjf_calibrated(lam=500.0, scoring=SCORING_PROFILE)
-    runp = lambda tr: simulate(tr, world, polp, capacity, svc, jct_profile=jprof)  # noqa: E731
-    resp = refine_qps(sweep_rates(trace, rates, seed=0, run=runp), slo,
-                      lambda q: sweep_rates(trace, [q], seed=0, run=runp)[0][1])
+    resp = refine_qps(sweep_rates(trace, rates, seed=0, run=sweep(polp, jprof)), slo,
+                      lambda q: sweep_rates(trace, [q], seed=0, run=sweep(polp, jprof))[0][1])
     best = pick(res, slo)
     rep = dict(res)[best] if best else None
+    # lambda sweep at one rate past the knee (the reference's `lambda-sweep`, ps/cli.py:213-252): the fairness
+    # weight trades mean latency (SRJF) against the p99 of the long cold requests (FIFO)
+    lam_rate = 1.1 * best if best else sat
+    arrived = wl.poisson_arrivals(trace, lam_rate, seed=0, keep_sessions=True)
+    lam_sweep = []
+    for lam in (0.0, 0.5, 5.0, 50.0, 500.0, 5000.0):
+        r = run(arrived, Policy.srjf_calibrated(lam=lam))
+        lam_sweep.append({"lambda": lam, "scoring": "proxy (miss tokens)", "p99_s": r.p99_latency,
+                          "mean_s": r.mean_latency})
+    for lam in (0.0, 0.5, 500.0):
+        r = run(arrived, Policy.srjf_calibrated(lam=lam, scoring=SCORING_PROFILE), jprof)
+        lam_sweep.append({"lambda": lam, "scoring": "profile (seconds)", "p99_s": r.p99_latency,
+                          "mean_s": r.mean_latency})
+    rf = run(arrived, Policy.fifo())
+    lam_sweep.append({"policy": "fifo", "p99_s": rf.p99_latency, "mean_s": rf.mean_latency})
+    # wall clock at the knee: real arrivals, the Server's worker thread and the C-ABI forward in the latency
+    wall = None
+    if best:
+        if world > 1:
+            dist.barrier()
+        arrived_knee = wl.poisson_arrivals(trace, best, seed=0, keep_sessions=True)
+        srv = Server([eng], Policy.srjf_calibrated())
+        try:
+            wrep = merged(replay(srv, shard_trace(arrived_knee, rank, world), ALLOWED))
+        finally:
+            srv.close()
+        wall = {"rate": best, "p99_s": wrep.p99_latency, "mean_s": wrep.mean_latency,
+                "throughput_rps": wrep.throughput, "served": wrep.served,
+                "note": "serving.Server + replay: arrivals injected in real time, wall-clock latency"}
     hits = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc > 0)
     colds = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc == 0)
+    if rank != 0:
+        return None
     return {
         "value": best, "unit": "requests/s", "slo_p99_s": slo, "n_gpus": world,
         "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
         "miss_tokens_per_s_at_slo": rep.miss_tokens_per_s if rep else None,
         "p99_at_value_s": rep.p99_latency if rep else None,
-        "fifo_qps_at_slo": pick(fifo, slo), "lambda500_qps_at_slo": pick(res500, slo),
+        "fifo_qps_at_slo": pick(fifo, slo),
         "profile_lambda500_qps_at_slo": pick(resp, slo),
+        "wall_clock_at_value": wall,
+        "lambda_sweep": {"rate": lam_rate, "runs": lam_sweep},
         "jct_profile": {"coef_input": jprof.coef_input, "coef_cached": jprof.coef_cached,
                         "intercept": jprof.intercept, "fit_r2": jprof.fit_r2},
         "saturation_rps": sat,
@@ -655,10 +698,10 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         "workload": "post-recommendation 40 users x 50 requests, profiles 19,850 +- 3,000 tokens + 150-token "
                     "suffix, Poisson arrivals (user sessions contiguous), Yes/No allowed ids",
         "method": f"virtual-clock serving loop with the reference's event semantics (calibrated SRJF, prefix pool of "
-                  f"{capacity} tokens per GPU, sticky routing over {world} replica(s)); every request of the "
-                  f"saturation run executed for real on GPU 0 in serving order and its device time reused by the "
-                  f"rate sweep (shapes the sweep meets beyond those: one forward each); {svc.forwards} real forwards "
-                  f"({time.perf_counter() - t0:.1f} s wall)",
+                  f"{capacity} tokens per GPU); each of the {world} rank(s) serves its sticky-routed shard on its own "
+                  f"GPU (saturation run executed for real in serving order, device times reused by the rate sweep; "
+                  f"shapes beyond those: one forward each), records merged over ranks; rank 0: {svc.forwards} real "
+                  f"forwards ({time.perf_counter() - t0:.1f} s wall)",
         "measured_service_s": {"cold_median": statistics.median(colds) if colds else None,
                                "prefix_hit_median": statistics.median(hits) if hits else None},
     }

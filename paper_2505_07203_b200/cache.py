@@ -171,32 +171,39 @@ class PrefixCache:
         return adm.stored_blocks * self.config.block_tokens
 
     def begin_insert(self, chain: Sequence[bytes], now: float) -> Admission:
+        """Plan an insertion (ps/cache.py:143-159): the resident prefix is found by the prefix-closed binary search,
+        then the suffix blocks are admitted (evicting LRU leaves off the path) until one cannot be.
+
+        Last-use stamps are kept lazily: an insertion stamps only its deepest stored block, and a block that loses
+        its last child takes the child's stamp if it is later (`_remove`). Only leaves are eviction candidates, and
+        a leaf's lazy stamp equals the reference's eager one (the latest insertion whose path ran through it), so
+        victims and tie-breaks are identical while an insertion costs O(new blocks) instead of O(chain)."""
         if self._pending is not None:
             raise CacheError("an insertion is already in flight on this instance")
         self.version += 1
         self._maybe_compact()
         chain = list(chain)
-        path = set(chain)
-        adm = Admission(chain=chain, stored_blocks=0)
+        n_res = self.match_chain(chain) // self.config.block_tokens
+        adm = Admission(chain=chain, stored_blocks=n_res)
         cap = self.config.capacity_blocks
-        for i, d in enumerate(chain):
-            node = self._blocks.get(d)
-            if node is not None:
-                self._stamp(d, node, now)
-                adm.touched.append(d)
-                adm.stored_blocks = i + 1
-                continue
+        path = None
+        for i in range(n_res, len(chain)):
+            d = chain[i]
             if len(self._blocks) >= cap:
+                if path is None:
+                    path = set(chain)
                 victim = self._evict_one(path)
                 if victim is None:
                     break  # this block and the whole suffix are discarded
                 adm.evicted[victim[0]] = victim[1]
-            parent = chain[i - 1] if i > 0 else None
-            slot = self._add_block(d, parent, now)
+            slot = self._add_block(d, chain[i - 1] if i > 0 else None, now)
             adm.admit.append((i, slot))
             adm.new_set.add(d)
-            adm.touched.append(d)
             adm.stored_blocks = i + 1
+        if adm.stored_blocks:
+            d = chain[adm.stored_blocks - 1]
+            self._stamp(d, self._blocks[d], now)
+            adm.touched.append(d)
         self._pending = adm
         return adm
 
@@ -204,7 +211,9 @@ class PrefixCache:
         """Finish an insertion: stamp the path with the completion time (the reference inserts at completion)."""
         if adm is not self._pending:
             raise CacheError("commit of an admission that is not in flight")
-        for d in adm.touched:
+        # the deepest stored block and the newly admitted ones (so a two-phase insertion leaves the same stamps as a
+        # one-shot insertion at the completion time)
+        for d in adm.touched + [adm.chain[b] for b, _ in adm.admit]:
             node = self._blocks.get(d)
             if node is not None and node.last_use != now:
                 self._stamp(d, node, now)
@@ -291,6 +300,8 @@ class PrefixCache:
         if node.parent is not None:
             p = self._blocks[node.parent]
             p.children -= 1
+            if node.last_use > p.last_use:  # lazy path stamps (begin_insert)
+                p.last_use = node.last_use
             if p.children == 0:
                 heapq.heappush(self._leaf_heap, (p.last_use, p.ins_order, node.parent))
         return node
