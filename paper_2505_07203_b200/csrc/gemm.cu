@@ -178,8 +178,16 @@ struct Pair {
 }  // namespace
 
 // F8: E4M3 operands (kind::f8f6f4); a k-block is still one 128-byte row per operand row (128 elements instead of 64)
-template <int EPI, int BNT, bool F8 = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+// EW: epilogue warps per TMEM lane quadrant (1: warps 4..7 drain whole tiles; 2: warps 4..11, each pair of warps of a
+// quadrant splits the tile's columns in 128-column halves). EW = 2 measured slower on the 20k step (QKV 24.4 -> 29.8
+// ms, O-proj 21.8 -> 21.3 ms: the O-proj is not bound by its epilogue warps' issue rate), so every variant uses 1.
+template <int EW>
+constexpr int pair_threads() { return 128 + 128 * EW; }
+template <bool F8, int BNT>
+constexpr int pair_ew() { return 1; }
+
+template <int EPI, int BNT, bool F8 = false, int EW = pair_ew<F8, BNT>()>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const GemmArgs args) {
   constexpr int KE = F8 ? 2 * BK : BK;  // k elements per k-block
@@ -286,6 +294,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp >= 4) {
     const int wq = warp & 3;
+    constexpr int CW = BNT / EW;  // columns per epilogue warp of a quadrant
+    const int part = (warp - 4) >> 2;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
     int it = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
@@ -297,9 +307,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row = mb * 2 * BM + rank * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BNT;
-      epilogue_tile<EPI, BNT, F8>(args, taddr, row, nb, ksp, t);
+      epilogue_tile<EPI, BNT, F8>(args, taddr, row, nb, ksp, t, PartSrc{}, part * CW, (part + 1) * CW);
       tc_fence_before();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 128 * EW);
       if (threadIdx.x == 128) mbar_arrive_cluster(tempty0 + acc * 8);
     }
   }
@@ -459,7 +469,7 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
   }
   const int tiles = tiles_mn * args.k_splits;
   const int npairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  launch_pdl(gemm2_kernel<EPI, BNT, F8>, dim3(2 * npairs), dim3(NUM_THREADS), Pair<BNT>::SMEM, stream, map_a, map_b2,
+  launch_pdl(gemm2_kernel<EPI, BNT, F8>, dim3(2 * npairs), dim3(pair_threads<pair_ew<F8, BNT>()>()), Pair<BNT>::SMEM, stream, map_a, map_b2,
              args);
   if (args.k_splits > 1) {
     const long long total = (long long)args.M * (args.N / 4);

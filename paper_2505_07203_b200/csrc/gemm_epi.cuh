@@ -153,9 +153,11 @@ __device__ __forceinline__ void dequant32(const GemmArgs& a, float as, int col0,
 }
 
 // Epilogue of one 128-row x 256-column accumulator (this thread: TMEM lane = output row `row`).
+// Columns [c_lo, c_hi) of the tile (a multiple of 128 wide and 128-aligned when the work is shared between several
+// warps of one TMEM lane quadrant): the default is the whole tile.
 template <int EPI, int BNT = 256, bool F8 = false, bool PART = false>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t taddr, int row, int nb, int ksp, int t,
-                                              const PartSrc& ps = PartSrc{}) {
+                                              const PartSrc& ps = PartSrc{}, int c_lo = 0, int c_hi = BNT) {
   const bool prow = PART && row < args.M;  // partial tiles hold rows < M only
   const float as = (F8 && row < args.M) ? args.a_scale[row] : 0.f;
   if (ksp > 1) {
@@ -164,7 +166,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
     pa.out = args.split_ws + (size_t)(t % ksp) * args.M * args.N;
     pa.ldo = args.N;
 #pragma unroll 1
-    for (int c = 0; c < BNT; c += 32) {
+    for (int c = c_lo; c < c_hi; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
@@ -174,7 +176,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
     // two 128-column heads per tile; rotate-half pairs (i, i+64)
     const float sc = (args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
 #pragma unroll 1
-    for (int h = 0; h < BNT / 128; ++h) {
+    for (int h = c_lo / 128; h < c_hi / 128; ++h) {
       const int hcol = nb * BNT + h * 128;
       const bool rot = hcol < args.rope_cols;
       const float2* cs = args.rope + (long long)(args.pos_offset + row) * 64;
@@ -228,7 +230,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
   } else if constexpr (EPI == EPI_RESID_F32) {
     float sq[2] = {0.f, 0.f};
 #pragma unroll 1
-    for (int c = 0; c < BNT; c += 32) {
+    for (int c = c_lo; c < c_hi; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
@@ -237,13 +239,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
       if (row < args.M) sq[c >> 7] += epilogue_chunk<EPI>(args, row, nb * BNT + c, r);
     }
     if (args.ss_out && row < args.M) {
-#pragma unroll
-      for (int k = 0; k < BNT / 128; ++k) args.ss_out[(long long)row * args.ss_nseg + nb * (BNT / 128) + k] = sq[k];
+      for (int k = c_lo / 128; k < c_hi / 128; ++k)
+        args.ss_out[(long long)row * args.ss_nseg + nb * (BNT / 128) + k] = sq[k];
     }
   } else {
     const float sc = (EPI == EPI_SILU_MUL && args.ss_in && row < args.M) ? row_inv_rms(args, row) : 1.0f;
 #pragma unroll 1
-    for (int c = 0; c < BNT; c += 32) {
+    for (int c = c_lo; c < c_hi; c += 32) {
       uint32_t r[32];
       tmem_ld32(taddr + c, r);
       tmem_ld_wait();
