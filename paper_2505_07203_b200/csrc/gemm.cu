@@ -234,7 +234,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
   cluster_sync();  // peer barriers initialised before any remote arrive / TMA completion
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
+  // The producer streams its first STAGES2 weight k-blocks before waiting for the previous kernel (weights are
+  // constant; only the activation rows depend on it), so the weight fetch overlaps the predecessor's tail.
+  if (warp != 0) pdl_wait();
   pdl_trigger();
 
   if (warp == 0) {
@@ -242,21 +244,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
       const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);  // leader's full_bar[0]
       int s = 0;
       uint32_t ph = 0;
+      int pend_s[STAGES2], pend_kb[STAGES2], pend_row[STAGES2];
+      int npend = 0;
+      bool open = false;
+      auto flush = [&]() {
+        pdl_wait();
+        open = true;
+        for (int i = 0; i < npend; ++i)
+          tma_load_2d_pair(sA + pend_s[i] * HALF_BYTES, &map_a, full0 + pend_s[i] * 8, pend_kb[i] * KE, pend_row[i]);
+        npend = 0;
+      };
       for (int t = pair; t < num_tiles; t += npairs) {
         int mb, nb;
         tile_coords(t / ksp, num_m, num_n, mb, nb);
         const int kb0 = (t % ksp) * kbps;
         const int nk = min(nk_total, kb0 + kbps) - kb0;
+        const int arow = args.a_row0 + mb * 2 * BM + rank * BM;
         for (int k = 0; k < nk; ++k) {
           const int kb = kb0 + k;
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * Pair<BNT>::STAGE);
           const uint32_t fb = full0 + s * 8;
-          tma_load_2d_pair(sA + s * HALF_BYTES, &map_a, fb, kb * KE, args.a_row0 + mb * 2 * BM + rank * BM);
           tma_load_2d_pair(sB + s * B_HALF, &map_b, fb, kb * KE, nb * BNT + rank * (BNT / 2));
+          if (open) {
+            tma_load_2d_pair(sA + s * HALF_BYTES, &map_a, fb, kb * KE, arow);
+          } else {
+            pend_s[npend] = s;
+            pend_kb[npend] = kb;
+            pend_row[npend] = arow;
+            if (++npend == STAGES2) flush();
+          }
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
       }
+      if (!open) flush();
     }
     __syncwarp();
   } else if (warp == 1) {
