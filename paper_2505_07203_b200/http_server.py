@@ -6,6 +6,16 @@ PAPER.md:403-409). The reference has no server; this is a thin FastAPI layer ove
                       "latency_s": 0.013, "service_s": 0.012}
   GET  /v1/stats     served requests, mean / p99 latency, prefix-hit counts (RequestRecord fields)
 
+OpenAI-compatible surface (the paper's vLLM-based front end speaks the OpenAI API; prefill-only means exactly one
+generated token, chosen among the allowed ids):
+  POST /v1/completions  {"model": "...", "prompt": "..." | [ids], "max_tokens": 1,
+                         "allowed_token_ids": [9642, 2822]  (vLLM's SamplingParams name)
+                         or "logit_bias": {"9642": 100, "2822": 100}  (the OpenAI way: ids with a bias >= 100
+                         are the allowed set), "logprobs": k, "user": "..."}
+                     -> {"object": "text_completion", "choices": [{"text", "token_ids", "logprobs", "finish_reason"}],
+                         "usage": {"prompt_tokens", "completion_tokens": 1, "prompt_tokens_details": {"cached_tokens"}}}
+  GET  /v1/models
+
 No tokenizer assets are available offline: "prompt" text is encoded as its UTF-8 bytes (token id = byte),
 which is enough for prefix sharing to behave like real prompts; pass "tokens" for real tokenizer ids.
 
@@ -42,8 +52,22 @@ try:  # pydantic / fastapi are optional at import time (the engine does not need
         tokens: list[int] | None = None
         prompt: str | None = None
         allowed: list[int]
+    class CompletionBody(BaseModel):
+        model: str | None = None
+        prompt: str | list[int]
+        max_tokens: int = 1
+        allowed_token_ids: list[int] | None = None
+        logit_bias: dict[str, float] | None = None
+        logprobs: int | None = None
+        user: str | int | None = None
 except ImportError:  # pragma: no cover
     PrefillBody = None
+    CompletionBody = None
+
+
+def _token_text(tid: int) -> str:
+    """Offline stand-in for detokenisation: byte ids decode as their byte, other ids as <id>."""
+    return bytes([tid]).decode("latin-1") if 0 <= tid < 256 else f"<{tid}>"
 
 
 def create_app(server):
@@ -84,6 +108,52 @@ def create_app(server):
         return {"id": rid, "token": res.token, "index": res.index, "probs": res.probs.tolist(),
                 "logits": res.logits.tolist(), "n_cached": res.n_cached,
                 "latency_s": time.perf_counter() - t0, "service_s": res.service_s}
+
+    model_name = getattr(getattr(server.workers[0].engine, "model", None), "name", "prefillonly")
+    users: dict = {}
+
+    @app.get("/v1/models")
+    def models():
+        return {"object": "list", "data": [{"id": model_name, "object": "model", "owned_by": "prefillonly-b200"}]}
+
+    @app.post("/v1/completions")
+    def completions(body: CompletionBody):
+        if body.max_tokens != 1:
+            raise HTTPException(400, "prefill-only serving produces exactly one token: max_tokens must be 1")
+        allowed = body.allowed_token_ids
+        if allowed is None and body.logit_bias:
+            allowed = [int(k) for k, v in body.logit_bias.items() if v >= 100]
+        if not allowed:
+            raise HTTPException(400, "give allowed_token_ids, or logit_bias with +100 on the allowed ids")
+        raw = body.prompt if isinstance(body.prompt, list) else list(body.prompt.encode("utf-8"))
+        if not raw:
+            raise HTTPException(400, "empty prompt")
+        if min(raw) < 0 or max(raw) >= 2 ** 32:
+            raise HTTPException(400, "token ids must be in [0, 2^32)")
+        vocab = getattr(getattr(server.workers[0].engine, "model", None), "vocab", None)
+        if min(allowed) < 0 or (vocab is not None and max(allowed) >= vocab):
+            raise HTTPException(400, f"allowed ids must be in [0, {vocab})")
+        with lock:
+            rid = next(ids)
+            uid = users.setdefault(body.user, len(users)) if body.user is not None else rid
+        try:
+            res = server.submit(_HttpRequest(rid, uid, np.asarray(raw, dtype=np.uint32)), allowed).result()
+        except ValueError as err:
+            raise HTTPException(413 if "exceeds" in str(err) else 400, str(err)) from None
+        except PrefillOnlyError as err:
+            raise HTTPException(400 if err.code in (_lib.PO_ERR_ARG, _lib.PO_ERR_POOL) else 500, str(err)) from None
+        logp = np.log(np.maximum(res.probs.astype(np.float64), 1e-45))
+        choice = {"index": 0, "text": _token_text(res.token), "token_ids": [res.token], "finish_reason": "length"}
+        if body.logprobs:
+            order = np.argsort(-logp, kind="stable")[: body.logprobs]
+            choice["logprobs"] = {"tokens": [_token_text(res.token)], "token_logprobs": [float(logp[res.index])],
+                                  "top_logprobs": [{_token_text(allowed[i]): float(logp[i]) for i in order}],
+                                  "allowed_token_ids": list(allowed), "allowed_probs": res.probs.tolist()}
+        n = len(raw)
+        return {"id": f"cmpl-{rid}", "object": "text_completion", "created": int(time.time()), "model": model_name,
+                "choices": [choice],
+                "usage": {"prompt_tokens": n, "completion_tokens": 1, "total_tokens": n + 1,
+                          "prompt_tokens_details": {"cached_tokens": res.n_cached}}}
 
     @app.get("/v1/stats")
     def stats():
