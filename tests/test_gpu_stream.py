@@ -70,3 +70,37 @@ def test_stream_gemm_repeatable():
     a, _ = run(A, B)
     b, _ = run(A, B)
     assert torch.equal(a, b)
+
+
+def test_engine_with_streaming_kernel_matches_oracle():
+    """The engine's opt-in streaming path (PO_STREAM=1: prefix hits' layer GEMMs as phases of stream_kernel) gives the
+    oracle's answers, in a fresh process (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r'''
+import numpy as np
+from oracle import llama_ref
+from paper_2505_07203_b200.config import ModelConfig
+from paper_2505_07203_b200.engine import Engine
+SMALL = ModelConfig("small", 2, 1024, 8, 2, 128, 2816, 4096)
+cfg = llama_ref.Cfg.from_model(SMALL)
+w = llama_ref.make_weights(cfg, 7)
+toks = np.random.default_rng([70, 0, 0]).integers(0, 2 ** 32, size=1600, dtype=np.uint32)
+slots = list(range(100))
+with Engine(SMALL, seed=7, max_tokens=2048, chunk=1024, pool_blocks=256) as e:
+    e.prefill(toks[:1344], [5, 11, 4095], 0, slots[:84])
+    for nc, n in ((1344, 1504), (1344, 1600), (1584, 1600), (0, 200), (0, 1)):
+        res = e.prefill(toks[:n], [5, 11, 4095], nc, slots[: n // 16])
+        logits, _, am = llama_ref.llama_forward(cfg, w, toks[:n], [5, 11, 4095])
+        err = np.abs(res.logits - logits).max()
+        assert err <= 1e-2 + 5e-3 * np.abs(logits).max(), (n, nc, err)
+        assert res.index == am, (n, nc)
+print("ok")
+'''
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PO_STREAM="1", PYTHONPATH=str(root))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
