@@ -131,6 +131,21 @@ int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached
                int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
                float* out_probs, int32_t* out_argmax, void* stream);
 
+/* po_prefill split in two, so a serving loop can take its next scheduling decision while this forward runs
+ * (ps/sim.py:217-229 decides at completion; serving.Server's lookahead decides one request ahead).
+ * po_prefill_submit validates and stages the request (host buffers are copied; the caller may reuse them on
+ * return), enqueues the forward on `stream` and returns a ticket. po_prefill_query sets *done when the ticket's
+ * forward and output copies have completed; po_prefill_wait blocks until then and copies the outputs
+ * (service_ms: device time of the forward incl. its H2D/D2H copies; may be NULL). Staging rotates over 4 entries:
+ * at most 3 tickets may be outstanding, a ticket's outputs are lost once 4 newer submits have recycled its entry
+ * (wait/query then return PO_ERR_ARG). po_prefill == submit + wait. */
+int po_prefill_submit(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
+                      int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, int64_t* ticket,
+                      void* stream);
+int po_prefill_query(po_engine* e, int64_t ticket, int32_t* done);
+int po_prefill_wait(po_engine* e, int64_t ticket, float* out_logits, float* out_probs, int32_t* out_argmax,
+                    float* service_ms);
+
 /* Same forward on device-resident inputs (d_tokens: all n uint32 ids; d_allowed: n_allowed ids) with device
  * outputs; asynchronous on `stream` (NULL = the engine's stream, see po_engine_stream). pool_block_ids is a
  * host array as in po_prefill. Used to time the hot path with inputs already in HBM. */

@@ -48,6 +48,9 @@ SIGNATURES = {
     "po_free": (_I32, [_VP]),
     "po_prefill": (_I32, [_VP, _VP, _I32, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "po_last_service_ms": (_I32, [_VP, _VP]),
+    "po_prefill_submit": (_I32, [_VP, _VP, _I32, _I32, _VP, _I32, _VP, _I32, _VP, _VP]),
+    "po_prefill_query": (_I32, [_VP, _I64, _VP]),
+    "po_prefill_wait": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP]),
     "po_prefill_device": (_I32, [_VP, _VP, _I32, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "po_engine_stream": (_I32, [_VP, _VP]),
     "po_last_launches": (_I32, [_VP, _VP]),

@@ -85,7 +85,19 @@ struct po_engine {
   int* ring_d_slots[STAGE_RING] = {};
   int* ring_d_kvslot[STAGE_RING] = {};
   cudaEvent_t ring_ev[STAGE_RING] = {};
+  // per entry: the request's pinned token / allowed-id staging, its pinned outputs, device-time events and the
+  // ticket of the po_prefill_submit that owns it (po_prefill_wait reads the outputs back through the ticket)
+  uint32_t* ring_h_tokens[STAGE_RING] = {};
+  int* ring_h_allowed[STAGE_RING] = {};
+  float* ring_h_logits[STAGE_RING] = {};
+  float* ring_h_probs[STAGE_RING] = {};
+  int* ring_h_argmax[STAGE_RING] = {};
+  cudaEvent_t ring_ev0[STAGE_RING] = {}, ring_ev1[STAGE_RING] = {};
+  int64_t ring_ticket[STAGE_RING] = {};
+  int ring_n_allowed[STAGE_RING] = {};
   int ring_next = 0;
+  int cur_ring = 0;  // entry of the request being staged
+  int64_t next_ticket = 0;
   int* d_allowed = nullptr;
   float* d_logits = nullptr;
   float* d_probs = nullptr;
@@ -203,16 +215,18 @@ int po_free(po_engine* e) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
   }
   for (void* p : e->allocs) cudaFree(p);
-  cudaFreeHost(e->h_tokens);
   for (int i = 0; i < po_engine::STAGE_RING; ++i) {
     cudaFreeHost(e->ring_h_slots[i]);
     cudaFreeHost(e->ring_h_kvslot[i]);
+    cudaFreeHost(e->ring_h_tokens[i]);
+    cudaFreeHost(e->ring_h_allowed[i]);
+    cudaFreeHost(e->ring_h_logits[i]);
+    cudaFreeHost(e->ring_h_probs[i]);
+    cudaFreeHost(e->ring_h_argmax[i]);
     if (e->ring_ev[i]) cudaEventDestroy(e->ring_ev[i]);
+    if (e->ring_ev0[i]) cudaEventDestroy(e->ring_ev0[i]);
+    if (e->ring_ev1[i]) cudaEventDestroy(e->ring_ev1[i]);
   }
-  cudaFreeHost(e->h_allowed);
-  cudaFreeHost(e->h_logits);
-  cudaFreeHost(e->h_probs);
-  cudaFreeHost(e->h_argmax);
   for (auto& pr : e->prof_events) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -402,7 +416,11 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     if (dalloc(e, &e->ring_d_slots[i], (size_t)max_blocks * 4, &e->arena_bytes) ||
         dalloc(e, &e->ring_d_kvslot[i], (size_t)max_blocks * 4, &e->arena_bytes) ||
         halloc(&e->ring_h_slots[i], (size_t)max_blocks * 4) || halloc(&e->ring_h_kvslot[i], (size_t)max_blocks * 4) ||
-        cudaEventCreateWithFlags(&e->ring_ev[i], cudaEventDisableTiming) != cudaSuccess)
+        halloc(&e->ring_h_tokens[i], (size_t)T * 4) || halloc(&e->ring_h_allowed[i], (size_t)c.vocab * 4) ||
+        halloc(&e->ring_h_logits[i], (size_t)c.vocab * 4) || halloc(&e->ring_h_probs[i], (size_t)c.vocab * 4) ||
+        halloc(&e->ring_h_argmax[i], 16) ||
+        cudaEventCreateWithFlags(&e->ring_ev[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreate(&e->ring_ev0[i]) != cudaSuccess || cudaEventCreate(&e->ring_ev1[i]) != cudaSuccess)
       return fail(PO_ERR_CUDA, "staging ring allocation failed");
   if (dalloc(e, &e->d_tokens, (size_t)T * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_allowed, (size_t)c.vocab * 4, &e->arena_bytes) ||
@@ -410,10 +428,6 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
       dalloc(e, &e->d_probs, (size_t)c.vocab * 4, &e->arena_bytes) ||
       dalloc(e, &e->d_argmax, 16, &e->arena_bytes))
     return fail(PO_ERR_CUDA, "staging allocation failed");
-  if (halloc(&e->h_tokens, (size_t)T * 4) || halloc(&e->h_allowed, (size_t)c.vocab * 4) ||
-      halloc(&e->h_logits, (size_t)c.vocab * 4) || halloc(&e->h_probs, (size_t)c.vocab * 4) ||
-      halloc(&e->h_argmax, 16))
-    return fail(PO_ERR_CUDA, "pinned host allocation failed");
   {
     const std::vector<float> inv = rope_inv_freq(c);
     const int half = c.head_dim / 2;
@@ -622,6 +636,12 @@ int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, 
   e->h_kvslot = e->ring_h_kvslot[ri];
   e->d_slots = e->ring_d_slots[ri];
   e->d_kvslot = e->ring_d_kvslot[ri];
+  e->h_tokens = e->ring_h_tokens[ri];
+  e->h_allowed = e->ring_h_allowed[ri];
+  e->h_logits = e->ring_h_logits[ri];
+  e->h_probs = e->ring_h_probs[ri];
+  e->h_argmax = e->ring_h_argmax[ri];
+  e->cur_ring = ri;
   // a fully cached request still recomputes its last token to produce logits
   const int n_c = n_cached < n ? n_cached : n - 1;
   const int cached_blocks = (n_c + bt - 1) / bt;
@@ -870,12 +890,6 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     if (l + 1 < L) rc |= qkv_gemm(l + 1);
   }
   rc |= flush();
-  // this request's staging-ring entry may be reused once everything enqueued so far has run
-  auto release_ring = [&] {
-    cudaEventRecord(e->ring_ev[e->ring_next], s);
-    e->ring_next = (e->ring_next + 1) % po_engine::STAGE_RING;
-  };
-  if (rc) release_ring();
   if (rc) return set_error(PO_ERR_CUDA, "po_prefill: kernel launch failed (%d): %s", rc,
                            cudaGetErrorString(cudaGetLastError()));
   mark(KC_LM_HEAD, true);
@@ -884,46 +898,103 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
   mark(KC_LM_HEAD, false);
   ++launches;
   e->last_launches = launches;
-  release_ring();
   if (cudaGetLastError() != cudaSuccess) return set_error(PO_ERR_CUDA, "po_prefill: launch error");
   return PO_OK;
 }
+
+// The staged request's ring entry may be reused once everything enqueued so far (its forward, table and output
+// copies) has run.
+void release_ring(po_engine* e, cudaStream_t s) {
+  cudaEventRecord(e->ring_ev[e->cur_ring], s);
+  e->ring_next = (e->cur_ring + 1) % po_engine::STAGE_RING;
+}
 }  // namespace
 
-int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
-               int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
-               float* out_probs, int32_t* out_argmax, void* stream) {
-  if (!e || !tokens || !allowed) return set_error(PO_ERR_ARG, "po_prefill: null argument");
+int po_prefill_submit(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
+                      int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, int64_t* ticket,
+                      void* stream) {
+  if (!e || !tokens || !allowed || !ticket) return set_error(PO_ERR_ARG, "po_prefill: null argument");
   const po_model_cfg& c = e->cfg;
-  int n_admit = 0;
-  const int n_c = stage_request(e, n, n_cached, n_allowed, pool_block_ids, n_blocks, &n_admit);
-  if (n_c < 0) return n_c;
   for (int i = 0; i < n_allowed; ++i)
     if (allowed[i] < 0 || allowed[i] >= c.vocab)
       return set_error(PO_ERR_ARG, "po_prefill: allowed id %d out of vocab", allowed[i]);
   cudaSetDevice(e->device);
+  int n_admit = 0;
+  const int n_c = stage_request(e, n, n_cached, n_allowed, pool_block_ids, n_blocks, &n_admit);
+  if (n_c < 0) return n_c;
+  const int ri = e->cur_ring;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
   const int n_miss = n - n_c;
   std::memcpy(e->h_tokens, tokens + n_c, (size_t)n_miss * 4);
   std::memcpy(e->h_allowed, allowed, (size_t)n_allowed * 4);
-  cudaEventRecord(e->ev0, s);
+  e->ring_ticket[ri] = -1;  // owned by nobody until the forward is enqueued
+  cudaEventRecord(e->ring_ev0[ri], s);
   cudaMemcpyAsync(e->d_tokens, e->h_tokens, (size_t)n_miss * 4, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(e->d_allowed, e->h_allowed, (size_t)n_allowed * 4, cudaMemcpyHostToDevice, s);
   const auto h0 = std::chrono::steady_clock::now();
   int rc = forward(e, e->d_tokens, n, n_c, n_admit, e->d_allowed, n_allowed, e->d_logits, e->d_probs, e->d_argmax, s);
-  if (rc) return rc;
+  if (rc) {
+    release_ring(e, s);
+    return rc;
+  }
   e->last_enqueue_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
   cudaMemcpyAsync(e->h_logits, e->d_logits, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(e->h_probs, e->d_probs, (size_t)n_allowed * 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(e->h_argmax, e->d_argmax, 4, cudaMemcpyDeviceToHost, s);
-  cudaEventRecord(e->ev1, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess)
-    return set_error(PO_ERR_CUDA, "po_prefill: forward failed: %s", cudaGetErrorString(cudaGetLastError()));
-  cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1);
-  if (out_logits) std::memcpy(out_logits, e->h_logits, (size_t)n_allowed * 4);
-  if (out_probs) std::memcpy(out_probs, e->h_probs, (size_t)n_allowed * 4);
-  if (out_argmax) *out_argmax = *e->h_argmax;
+  cudaEventRecord(e->ring_ev1[ri], s);
+  release_ring(e, s);
+  if (cudaGetLastError() != cudaSuccess) return set_error(PO_ERR_CUDA, "po_prefill: launch error");
+  e->ring_n_allowed[ri] = n_allowed;
+  e->ring_ticket[ri] = *ticket = ++e->next_ticket;
   return PO_OK;
+}
+
+namespace {
+int ring_of(po_engine* e, int64_t ticket) {
+  for (int i = 0; i < po_engine::STAGE_RING; ++i)
+    if (e->ring_ticket[i] == ticket && ticket > 0) return i;
+  return -1;
+}
+}  // namespace
+
+int po_prefill_query(po_engine* e, int64_t ticket, int32_t* done) {
+  if (!e || !done) return set_error(PO_ERR_ARG, "po_prefill_query: null argument");
+  const int ri = ring_of(e, ticket);
+  if (ri < 0) return set_error(PO_ERR_ARG, "po_prefill_query: unknown or recycled ticket %lld", (long long)ticket);
+  const cudaError_t q = cudaEventQuery(e->ring_ev1[ri]);
+  if (q != cudaSuccess && q != cudaErrorNotReady)
+    return set_error(PO_ERR_CUDA, "po_prefill: forward failed: %s", cudaGetErrorString(q));
+  *done = q == cudaSuccess;
+  return PO_OK;
+}
+
+int po_prefill_wait(po_engine* e, int64_t ticket, float* out_logits, float* out_probs, int32_t* out_argmax,
+                    float* service_ms) {
+  if (!e) return set_error(PO_ERR_ARG, "po_prefill_wait: null engine");
+  const int ri = ring_of(e, ticket);
+  if (ri < 0) return set_error(PO_ERR_ARG, "po_prefill_wait: unknown or recycled ticket %lld", (long long)ticket);
+  if (cudaEventSynchronize(e->ring_ev1[ri]) != cudaSuccess)
+    return set_error(PO_ERR_CUDA, "po_prefill: forward failed: %s", cudaGetErrorString(cudaGetLastError()));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ring_ev0[ri], e->ring_ev1[ri]);
+  e->last_ms = ms;
+  if (service_ms) *service_ms = ms;
+  const int na = e->ring_n_allowed[ri];
+  if (out_logits) std::memcpy(out_logits, e->ring_h_logits[ri], (size_t)na * 4);
+  if (out_probs) std::memcpy(out_probs, e->ring_h_probs[ri], (size_t)na * 4);
+  if (out_argmax) *out_argmax = *e->ring_h_argmax[ri];
+  e->ring_ticket[ri] = 0;  // consumed
+  return PO_OK;
+}
+
+int po_prefill(po_engine* e, const uint32_t* tokens, int32_t n, int32_t n_cached, const int32_t* allowed,
+               int32_t n_allowed, const int32_t* pool_block_ids, int32_t n_blocks, float* out_logits,
+               float* out_probs, int32_t* out_argmax, void* stream) {
+  int64_t ticket = 0;
+  if (int rc = po_prefill_submit(e, tokens, n, n_cached, allowed, n_allowed, pool_block_ids, n_blocks, &ticket,
+                                 stream))
+    return rc;
+  return po_prefill_wait(e, ticket, out_logits, out_probs, out_argmax, nullptr);
 }
 
 int po_prefill_device(po_engine* e, const uint32_t* d_tokens, int32_t n, int32_t n_cached, const int32_t* d_allowed,
@@ -931,12 +1002,15 @@ int po_prefill_device(po_engine* e, const uint32_t* d_tokens, int32_t n, int32_t
                       float* d_probs, int32_t* d_argmax, void* stream) {
   if (!e || !d_tokens || !d_allowed || !d_logits || !d_probs || !d_argmax)
     return set_error(PO_ERR_ARG, "po_prefill_device: null argument");
+  cudaSetDevice(e->device);
   int n_admit = 0;
   const int n_c = stage_request(e, n, n_cached, n_allowed, pool_block_ids, n_blocks, &n_admit);
   if (n_c < 0) return n_c;
-  cudaSetDevice(e->device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
-  return forward(e, d_tokens + n_c, n, n_c, n_admit, d_allowed, n_allowed, d_logits, d_probs, d_argmax, s);
+  e->ring_ticket[e->cur_ring] = 0;
+  const int rc = forward(e, d_tokens + n_c, n, n_c, n_admit, d_allowed, n_allowed, d_logits, d_probs, d_argmax, s);
+  release_ring(e, s);
+  return rc;
 }
 
 int po_engine_stream(po_engine* e, void** stream) {

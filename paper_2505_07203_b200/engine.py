@@ -50,6 +50,15 @@ def _raise(err: _lib.PrefillOnlyError):
     raise err
 
 
+@dataclass(frozen=True)
+class Ticket:
+    """An enqueued request (Engine.prefill_submit)."""
+
+    id: int
+    allowed: np.ndarray
+    n_cached: int
+
+
 class Engine:
     """One GPU's PrefillOnly engine: weights, arena, one-layer KV buffer and the prefix-KV pool."""
 
@@ -112,25 +121,47 @@ class Engine:
         tokens: uint32 ids (embedded as id % vocab). n_cached: block-aligned prefix already in the pool,
         with pool_block_ids[b] its slots; later entries of pool_block_ids are admission slots (-1 = discard).
         """
+        return self.prefill_wait(self.prefill_submit(tokens, allowed, n_cached, pool_block_ids, stream))
+
+    def prefill_submit(self, tokens, allowed: Sequence[int], n_cached: int = 0,
+                       pool_block_ids: Sequence[int] | None = None, stream: int | None = None) -> "Ticket":
+        """Stage and enqueue one request (po_prefill_submit); returns at once with a ticket for prefill_wait.
+        At most three tickets may be outstanding per engine (the staging ring has four entries)."""
         toks = np.ascontiguousarray(tokens, dtype=np.uint32)
         alw = np.ascontiguousarray(allowed, dtype=np.int32)
         n = int(toks.shape[0])
         ids = np.ascontiguousarray(pool_block_ids if pool_block_ids is not None else [], dtype=np.int32)
-        logits = np.empty(len(alw), dtype=np.float32)
-        probs = np.empty(len(alw), dtype=np.float32)
-        argmax = ctypes.c_int32(-1)
-        lib = _lib.load()
-        rc = lib.po_prefill(self._h, toks.ctypes.data, n, int(n_cached), alw.ctypes.data, len(alw),
-                            ids.ctypes.data if len(ids) else None, len(ids), logits.ctypes.data, probs.ctypes.data,
-                            ctypes.addressof(argmax), stream)
+        t = ctypes.c_int64(0)
+        rc = _lib.load().po_prefill_submit(self._h, toks.ctypes.data, n, int(n_cached), alw.ctypes.data, len(alw),
+                                           ids.ctypes.data if len(ids) else None, len(ids), ctypes.addressof(t),
+                                           stream)
         try:
             _lib.check(rc)
         except _lib.PrefillOnlyError as err:
             _raise(err)
+        return Ticket(int(t.value), alw, int(n_cached))
+
+    def prefill_done(self, ticket: "Ticket") -> bool:
+        """Non-blocking: has the ticket's forward completed (po_prefill_query)?"""
+        done = ctypes.c_int32(0)
+        _lib.call("po_prefill_query", self._h, ticket.id, ctypes.addressof(done))
+        return bool(done.value)
+
+    def prefill_wait(self, ticket: "Ticket") -> PrefillResult:
+        """Block until the ticket's forward completed and return its result (po_prefill_wait)."""
+        alw = ticket.allowed
+        logits = np.empty(len(alw), dtype=np.float32)
+        probs = np.empty(len(alw), dtype=np.float32)
+        argmax = ctypes.c_int32(-1)
         ms = ctypes.c_float()
-        _lib.check(lib.po_last_service_ms(self._h, ctypes.addressof(ms)))
+        rc = _lib.load().po_prefill_wait(self._h, ticket.id, logits.ctypes.data, probs.ctypes.data,
+                                         ctypes.addressof(argmax), ctypes.addressof(ms))
+        try:
+            _lib.check(rc)
+        except _lib.PrefillOnlyError as err:
+            _raise(err)
         idx = int(argmax.value)
-        return PrefillResult(token=int(alw[idx]), index=idx, probs=probs, logits=logits, n_cached=int(n_cached),
+        return PrefillResult(token=int(alw[idx]), index=idx, probs=probs, logits=logits, n_cached=ticket.n_cached,
                              service_s=float(ms.value) * 1e-3)
 
     def prefill_device(self, d_tokens: int, n: int, d_allowed: int, n_allowed: int, d_logits: int, d_probs: int,

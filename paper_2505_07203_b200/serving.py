@@ -360,13 +360,31 @@ class _Job:
 
 
 class _Worker(threading.Thread):
-    def __init__(self, server: "Server", idx: int, engine):
+    """One engine's serving loop.
+
+    lookahead=False: decide, run, commit, repeat -- every decision is taken when the engine frees up, the
+    reference's event order (ps/sim.py:211-229), and the host-side work (schedule_next, cache probes, slot tables,
+    enqueueing the forward) sits between forwards with the GPU idle.
+    lookahead=True (default, engines with prefill_submit): up to two forwards in flight on the engine stream. As soon
+    as a forward is enqueued the loop takes the next decision (schedule_next, begin_insert, commit) and enqueues it
+    behind, so the host work of request i+1 overlaps the forward of request i and the GPU runs back to back. A
+    decision is then taken when its predecessor starts rather than when it completes: requests arriving during that
+    forward compete from the following decision on. The admission is committed at decision time; the predecessor's
+    forward (same stream) completes before this one's starts, so K/V it admits are in the pool when they are read,
+    and a slot this decision evicts is overwritten only after the predecessor has read it. One thread per engine:
+    the C-ABI calls release the GIL, and no second Python thread competes for it.
+    """
+
+    DEPTH = 2  # forwards in flight per engine (the staging ring holds 4)
+
+    def __init__(self, server: "Server", idx: int, engine, lookahead: bool = True):
         super().__init__(daemon=True, name=f"prefillonly-worker-{idx}")
         self.server, self.idx, self.engine = server, idx, engine
         self.inst = Instance(PrefixCache(CacheConfig(engine.capacity_tokens, engine.block_tokens)))
         self.jobs: dict = {}
         self.cv = threading.Condition()
         self.stop = False
+        self.lookahead = lookahead and hasattr(engine, "prefill_submit")
 
     def enqueue(self, job: _Job, now: float):
         with self.cv:
@@ -378,10 +396,30 @@ class _Worker(threading.Thread):
             self.inst.queue.append(job.wr)
             self.cv.notify()
 
+    def _decide(self, now: float):
+        """schedule_next + cache probe + admission (caller holds self.cv)."""
+        srv = self.server
+        bt = self.engine.block_tokens
+        wr = schedule_next(self.inst.queue, self.inst.cache, srv.jct_profile, srv.policy, now)
+        self.inst.queue.remove(wr)
+        job = self.jobs.pop(id(wr))
+        n_cached = self.inst.cache.match_chain(wr.chain)
+        ncb = n_cached // bt
+        slots = self.inst.cache.slots(wr.chain, ncb)
+        adm = self.inst.cache.begin_insert(wr.chain, now)
+        return wr, job, n_cached, adm.pool_block_ids(ncb, slots), adm
+
+    def _finish(self, wr, job, n_cached, res, start, done):
+        rec = RequestRecord(wr.request.id, wr.request.user_id, self.idx, wr.arrival, start, done,
+                            wr.request.n_input, n_cached, res.token)
+        self.server._record(rec)
+        job.future.set_result(res)
+
     def run(self):
+        if self.lookahead:
+            return self._pipelined()
         srv = self.server
         eng = self.engine
-        bt = eng.block_tokens
         while True:
             with self.cv:
                 while not self.inst.queue and not self.stop:
@@ -389,15 +427,9 @@ class _Worker(threading.Thread):
                 if self.stop and not self.inst.queue:
                     return
                 now = srv.clock()
-                wr = schedule_next(self.inst.queue, self.inst.cache, srv.jct_profile, srv.policy, now)
-                self.inst.queue.remove(wr)
-                job = self.jobs.pop(id(wr))
-                n_cached = self.inst.cache.match_chain(wr.chain)
-                ncb = n_cached // bt
-                slots = self.inst.cache.slots(wr.chain, ncb)
-                adm = self.inst.cache.begin_insert(wr.chain, now)
+                wr, job, n_cached, ids, adm = self._decide(now)
             try:
-                res = eng.prefill(wr.request.tokens, job.allowed, n_cached, adm.pool_block_ids(ncb, slots))
+                res = eng.prefill(wr.request.tokens, job.allowed, n_cached, ids)
             except Exception as exc:  # the forward failed: its admitted blocks hold no K/V
                 with self.cv:
                     self.inst.cache.abort(adm)
@@ -407,16 +439,73 @@ class _Worker(threading.Thread):
             with self.cv:
                 self.inst.cache.commit(adm, done)
                 self.inst.busy_time += done - now
-            rec = RequestRecord(wr.request.id, wr.request.user_id, self.idx, wr.arrival, now, done,
-                                wr.request.n_input, n_cached, res.token)
-            srv._record(rec)
-            job.future.set_result(res)
+            self._finish(wr, job, n_cached, res, now, done)
+
+    def _drop_admission(self, adm):
+        """A committed admission whose forward failed: its new blocks never received K/V."""
+        cache = self.inst.cache
+        for b, _ in reversed(adm.admit):
+            d = adm.chain[b]
+            if d in cache._blocks and cache._blocks[d].children == 0:
+                cache._remove(d)
+        cache.version += 1
+
+    def _pipelined(self):
+        srv = self.server
+        eng = self.engine
+        inflight: list = []  # [wr, job, n_cached, adm, ticket, t_submit], oldest first
+        last_done = 0.0
+        while True:
+            plan = None
+            with self.cv:
+                while not self.stop and not self.inst.queue and not inflight:
+                    self.cv.wait()
+                if self.stop and not self.inst.queue and not inflight:
+                    return
+                if self.inst.queue and len(inflight) < self.DEPTH:
+                    now = srv.clock()
+                    plan = self._decide(now)
+                    self.inst.cache.commit(plan[4], now)
+            if plan is not None:
+                wr, job, n_cached, ids, adm = plan
+                try:
+                    ticket = eng.prefill_submit(wr.request.tokens, job.allowed, n_cached, ids)
+                except Exception as exc:
+                    with self.cv:
+                        self._drop_admission(adm)
+                    job.future.set_exception(exc)
+                    continue
+                inflight.append([wr, job, n_cached, adm, ticket, now])
+                if len(inflight) < self.DEPTH:
+                    continue  # keep the engine fed: decide the next one while this forward runs
+            wr, job, n_cached, adm, ticket, t_sub = inflight[0]
+            if len(inflight) < self.DEPTH and not eng.prefill_done(ticket):
+                # one forward in flight and nothing to plan: wake on an arrival or poll the completion
+                with self.cv:
+                    if not self.inst.queue and not self.stop:
+                        self.cv.wait(timeout=2e-4)
+                continue
+            inflight.pop(0)
+            try:
+                res = eng.prefill_wait(ticket)
+            except Exception as exc:
+                with self.cv:
+                    self._drop_admission(adm)
+                job.future.set_exception(exc)
+                continue
+            done = srv.clock()
+            start = max(t_sub, last_done)  # it ran behind its predecessor on the engine stream
+            last_done = done
+            with self.cv:
+                self.inst.busy_time += done - start
+            self._finish(wr, job, n_cached, res, start, done)
 
 
 class Server:
     """Request-level data parallelism over engines (one per GPU), SRJF-calibrated by default."""
 
-    def __init__(self, engines: Sequence, policy: Policy | None = None, jct_profile: JctProfile | None = None):
+    def __init__(self, engines: Sequence, policy: Policy | None = None, jct_profile: JctProfile | None = None,
+                 lookahead: bool = True):
         if not engines:
             raise ServingError("need at least one engine")
         self.policy = policy or Policy.srjf_calibrated()
@@ -426,7 +515,7 @@ class Server:
         self._lock = threading.Lock()
         self.records: list = []
         self._memo: dict = {}
-        self.workers = [_Worker(self, i, e) for i, e in enumerate(engines)]
+        self.workers = [_Worker(self, i, e, lookahead) for i, e in enumerate(engines)]
         for w in self.workers:
             w.start()
 

@@ -36,19 +36,30 @@ def engine():
         yield e
 
 
-def test_server_on_gpu_matches_oracle_order_and_answers(engine):
+@pytest.mark.parametrize("lookahead", [False, True])
+def test_server_on_gpu_matches_oracle_order_and_answers(engine, lookahead):
+    """lookahead=False decides when the engine frees up; lookahead=True (prefill_submit / prefill_wait, two
+    forwards in flight) decides one request ahead. With every request queued before the first decision both take
+    the oracle's decisions."""
     gate = threading.Event()
-    orig = engine.prefill
+    orig_submit, orig_wait = engine.prefill_submit, engine.prefill_wait
     seen = {}
+    pending_toks = {}
 
-    def gated(tokens, allowed, n_cached=0, pool_block_ids=None):
+    def gated_submit(tokens, allowed, n_cached=0, pool_block_ids=None, stream=None):
         gate.wait()
-        res = orig(tokens, allowed, n_cached, pool_block_ids)
-        seen[len(seen)] = (np.asarray(tokens).copy(), n_cached, res)
+        t = orig_submit(tokens, allowed, n_cached, pool_block_ids, stream)
+        pending_toks[t.id] = (np.asarray(tokens).copy(), n_cached)
+        return t
+
+    def recording_wait(ticket):
+        res = orig_wait(ticket)
+        toks, nc = pending_toks.pop(ticket.id)
+        seen[len(seen)] = (toks, nc, res)
         return res
 
-    engine.prefill = gated
-    srv = Server([engine], Policy.srjf_calibrated(lam=0.0))
+    engine.prefill_submit, engine.prefill_wait = gated_submit, recording_wait
+    srv = Server([engine], Policy.srjf_calibrated(lam=0.0), lookahead=lookahead)
     try:
         tr = trace()
         futs = [srv.submit(r, YES_NO) for r in tr.requests]
@@ -57,7 +68,7 @@ def test_server_on_gpu_matches_oracle_order_and_answers(engine):
         results = [f.result(timeout=120) for f in futs]
     finally:
         srv.close()
-        engine.prefill = orig
+        del engine.prefill_submit, engine.prefill_wait
     assert len(results) == len(tr.requests) == 50
     assert all(r.token in YES_NO for r in results)
     order = [r.id for r in sorted(srv.records, key=lambda r: r.start)]
@@ -89,11 +100,35 @@ def test_server_on_gpu_matches_oracle_order_and_answers(engine):
         assert res.index == am
 
 
-def test_server_replay_on_gpu_in_real_time(engine):
-    srv = Server([engine], Policy.srjf_calibrated())
+@pytest.mark.parametrize("lookahead", [False, True])
+def test_server_replay_on_gpu_in_real_time(engine, lookahead):
+    srv = Server([engine], Policy.srjf_calibrated(), lookahead=lookahead)
     try:
         rep = replay(srv, wl.poisson_arrivals(trace(), 200.0, seed=2), YES_NO)
     finally:
         srv.close()
     assert rep.served == 50 and rep.cache_hit_requests >= 40
     assert rep.p99_latency > 0 and all(r.completion >= r.start >= r.arrival for r in rep.records)
+
+
+def test_submit_wait_back_to_back_hits_with_distinct_slot_tables(engine):
+    """Two prefix hits enqueued before either completes (staging ring): each reads its own pool slots."""
+    cfg = llama_ref.Cfg.from_model(TINY)
+    w = llama_ref.make_weights(cfg, 42)
+    rng = np.random.default_rng([5, 0, 0])
+    a = rng.integers(0, 2 ** 32, size=1200, dtype=np.uint32)
+    b = rng.integers(0, 2 ** 32, size=1200, dtype=np.uint32)
+    sa, sb = list(range(1000, 1075)), list(range(1500, 1575))
+    engine.prefill(a, YES_NO, 0, sa)
+    engine.prefill(b, YES_NO, 0, sb)
+    ta = engine.prefill_submit(a, YES_NO, 1184, sa)
+    tb = engine.prefill_submit(b, YES_NO, 1184, sb)
+    tc = engine.prefill_submit(a[:640], YES_NO, 0, [])
+    rb, ra, rc = engine.prefill_wait(tb), engine.prefill_wait(ta), engine.prefill_wait(tc)
+    for toks, res in ((a, ra), (b, rb), (a[:640], rc)):
+        logits, _, am = llama_ref.llama_forward(cfg, w, toks, YES_NO)
+        assert np.abs(res.logits - logits).max() <= 1e-2 + 5e-3 * np.abs(logits).max()
+        assert res.index == am
+    assert ra.n_cached == rb.n_cached == 1184 and ra.service_s > 0
+    with pytest.raises(Exception):
+        engine.prefill_wait(ta)  # consumed

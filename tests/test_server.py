@@ -100,3 +100,92 @@ def test_scheduling_decisions_match_oracle_shadow():
         cache.insert_chain(w["chain"], t)
         t += 1.0
     assert order == expected
+
+
+class AsyncFakeEngine(FakeEngine):
+    """Stand-in with the engine's asynchronous API: forwards run back to back on a virtual device timeline."""
+
+    def __init__(self, **kw):
+        super().__init__(**kw)
+        self.free_at = 0.0
+        self.max_inflight = 0
+        self.inflight = 0
+
+    def prefill_submit(self, tokens, allowed, n_cached=0, pool_block_ids=None):
+        n = len(tokens)
+        svc = 2e-3 + self.scale * (n - n_cached)
+        now = time.perf_counter()
+        self.free_at = max(now, self.free_at) + svc
+        with self.lock:
+            self.calls.append((n, n_cached, list(pool_block_ids or [])))
+            self.inflight += 1
+            self.max_inflight = max(self.max_inflight, self.inflight)
+        return (self.free_at, svc, allowed[0], n_cached)
+
+    def prefill_done(self, t):
+        return time.perf_counter() >= t[0]
+
+    def prefill_wait(self, t):
+        d = t[0] - time.perf_counter()
+        if d > 0:
+            time.sleep(d)
+        with self.lock:
+            self.inflight -= 1
+        return PrefillResult(token=t[2], index=0, probs=np.array([1.0, 0.0]), logits=np.zeros(2), n_cached=t[3],
+                             service_s=t[1])
+
+
+def test_lookahead_keeps_two_forwards_in_flight_and_reuses_prefixes():
+    eng = AsyncFakeEngine()
+    srv = Server([eng], Policy.srjf_calibrated())
+    assert srv.workers[0].lookahead
+    try:
+        rep = replay(srv, wl.poisson_arrivals(small_trace(), 2000.0, seed=1), [9642, 2822])
+    finally:
+        srv.close()
+    assert rep.served == 24 and rep.cache_hit_requests >= 16
+    assert eng.max_inflight == 2  # decided and enqueued while its predecessor ran
+    recs = sorted(rep.records, key=lambda r: r.start)
+    # back to back on the engine: no record starts before its predecessor completed
+    assert all(b.start >= a.completion - 1e-9 for a, b in zip(recs, recs[1:]))
+    for n, nc, ids in eng.calls:
+        assert nc % 16 == 0 and len(ids) == n // 16
+
+
+def test_lookahead_decisions_match_oracle_when_all_queued():
+    """Everything queued behind a blocked first submit: lookahead takes the same decisions as the oracle."""
+    eng = AsyncFakeEngine(scale=0.0)
+    gate = threading.Event()
+    orig = eng.prefill_submit
+
+    def gated(*a, **k):
+        gate.wait()
+        return orig(*a, **k)
+
+    eng.prefill_submit = gated
+    srv = Server([eng], Policy.srjf_calibrated(lam=0.0))
+    try:
+        trace = small_trace()
+        futs = [srv.submit(r, [1, 2]) for r in trace.requests]
+        time.sleep(0.2)
+        gate.set()
+        for f in futs:
+            f.result(timeout=30)
+    finally:
+        srv.close()
+    order = [r.id for r in sorted(srv.records, key=lambda r: (r.start, r.completion))]
+    cache = sched_ref.PrefixCache(eng.capacity_tokens)
+    pending = [dict(id=r.id, n_input=r.n_input, arrival=0.0, frozen_jct=0.0, chain=r.digest_chain(16, {}))
+               for r in trace.requests]
+    first = next(p for p in pending if p["id"] == order[0])
+    expected = [first["id"]]
+    pending.remove(first)
+    cache.insert_chain(first["chain"], 1.0)
+    t = 2.0
+    while pending:
+        w = sched_ref.schedule_next(pending, cache, "cal", t, lam=0.0)
+        expected.append(w["id"])
+        pending.remove(w)
+        cache.insert_chain(w["chain"], t)
+        t += 1.0
+    assert order == expected
