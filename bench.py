@@ -660,20 +660,34 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
                           "mean_s": r.mean_latency})
     rf = run(arrived, Policy.fifo())
     lam_sweep.append({"policy": "fifo", "p99_s": rf.p99_latency, "mean_s": rf.mean_latency})
-    # wall clock at the knee: real arrivals, the Server's worker thread and the C-ABI forward in the latency
+    # wall clock: serving.Server (lookahead loop, C-ABI forwards, host-side hashing / scheduling / copies inside the
+    # latency) with real arrivals in real time. First its saturation throughput (every request at t = 0), then the
+    # highest of {1.0, 0.95, 0.9, 0.85, 0.8} x the virtual-clock knee whose wall-clock p99 meets the SLO.
     wall = None
     if best:
-        if world > 1:
-            dist.barrier()
-        arrived_knee = wl.poisson_arrivals(trace, best, seed=0, keep_sessions=True)
-        srv = Server([eng], Policy.srjf_calibrated())
-        try:
-            wrep = merged(replay(srv, shard_trace(arrived_knee, rank, world), ALLOWED))
-        finally:
-            srv.close()
-        wall = {"rate": best, "p99_s": wrep.p99_latency, "mean_s": wrep.mean_latency,
-                "throughput_rps": wrep.throughput, "served": wrep.served,
-                "note": "serving.Server + replay: arrivals injected in real time, wall-clock latency"}
+        def wall_run(tr):
+            if world > 1:
+                dist.barrier()
+            srv = Server([eng], Policy.srjf_calibrated())
+            try:
+                return merged(replay(srv, shard_trace(tr, rank, world), ALLOWED))
+            finally:
+                srv.close()
+
+        wsat = wall_run(wl.zero_arrivals(trace))
+        runs = []
+        for m in (1.0, 0.95, 0.9, 0.85, 0.8):
+            q = best * m
+            wrep = wall_run(wl.poisson_arrivals(trace, q, seed=0, keep_sessions=True))
+            runs.append({"rate": q, "p99_s": wrep.p99_latency, "mean_s": wrep.mean_latency,
+                         "throughput_rps": wrep.throughput, "served": wrep.served})
+            if wrep.p99_latency <= slo:
+                break
+        ok = [r["rate"] for r in runs if r["p99_s"] <= slo]
+        wall = {"qps_at_slo": max(ok) if ok else None, "saturation_rps": wsat.throughput,
+                "virtual_saturation_rps": sat, "runs": runs,
+                "note": "serving.Server (lookahead: next decision while the current forward runs) + replay: arrivals "
+                        "injected in real time, wall-clock latency incl. host hashing, scheduling, staging copies"}
     hits = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc > 0)
     colds = sorted(v[0] for (rid, nc), v in svc.by_request.items() if nc == 0)
     if rank != 0:
@@ -685,7 +699,7 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
         "p99_at_value_s": rep.p99_latency if rep else None,
         "fifo_qps_at_slo": pick(fifo, slo),
         "profile_lambda500_qps_at_slo": pick(resp, slo),
-        "wall_clock_at_value": wall,
+        "wall_clock": wall,
         "lambda_sweep": {"rate": lam_rate, "runs": lam_sweep},
         "jct_profile": {"coef_input": jprof.coef_input, "coef_cached": jprof.coef_cached,
                         "intercept": jprof.intercept, "fit_r2": jprof.fit_r2},

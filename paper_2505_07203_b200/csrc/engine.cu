@@ -683,6 +683,10 @@ bool bounded_a_enabled();
 // zero-filled by TMA instead of being read from memory (for M = 1 that is 127 wasted rows per weight tile).
 int gemm(const CUtensorMap& a, const void* x, long long ldx, const CUtensorMap& b1, const CUtensorMap& b2,
          const CUtensorMap& b3, int epi, const po::GemmArgs& g, cudaStream_t s) {
+  if (po::gemm_swap_enabled() && g.M <= 256) {  // short launches: weight as the MMA's M operand
+    const int rc = po::gemm_launch_swap(b2, x, ldx, epi, g, s);
+    if (rc != 1) return rc;
+  }
   const CUtensorMap* am = &a;
   CUtensorMap bounded;
   if (g.M % 128 != 0 && bounded_a_enabled()) {

@@ -359,6 +359,20 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
   }
 }
 
+int splitk_reduce_launch(int epi, const GemmArgs& args, cudaStream_t stream) {
+  const long long total = (long long)args.M * (args.N / 4);
+  const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  switch (epi) {
+    case EPI_BF16: launch_pdl(splitk_reduce_kernel<EPI_BF16>, dim3(blocks), dim3(256), 0, stream, args); break;
+    case EPI_RESID_F32: launch_pdl(splitk_reduce_kernel<EPI_RESID_F32>, dim3(blocks), dim3(256), 0, stream, args); break;
+    case EPI_SILU_MUL: launch_pdl(splitk_reduce_kernel<EPI_SILU_MUL>, dim3(blocks), dim3(256), 0, stream, args); break;
+    case EPI_QKV_ROPE: launch_pdl(splitk_reduce_kernel<EPI_QKV_ROPE>, dim3(blocks), dim3(256), 0, stream, args); break;
+    case EPI_F32: launch_pdl(splitk_reduce_kernel<EPI_F32>, dim3(blocks), dim3(256), 0, stream, args); break;
+    default: return -3;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -401,6 +415,21 @@ int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t 
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// Plain (unswizzled) 3-D map for epilogue stores: dims {d0, d1, d2}, strides in bytes, fp32 or bf16 elements.
+int make_tmap_store_3d(CUtensorMap* map, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,
+                       uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -426,6 +455,8 @@ int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long 
   plan->M = M;
   plan->N = N;
   plan->K = K;
+  plan->A = A;
+  plan->lda = lda;
   if (make_tmap_2d_bf16(&plan->map_a, A, K, M, lda * 2, BK, BM)) return -2;
   if (make_tmap_2d_bf16(&plan->map_b, B, K, N, ldb * 2, BK, BN)) return -2;
   if (make_tmap_2d_bf16(&plan->map_b2, B, K, N, ldb * 2, BK, BM)) return -2;
@@ -679,6 +710,10 @@ int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t str
   args.M = plan.M;
   args.N = plan.N;
   args.K = plan.K;
+  if (gemm_swap_enabled() && args.M <= 256) {
+    const int rc = gemm_launch_swap(plan.map_b2, plan.A, plan.lda, epi, args, stream);
+    if (rc != 1) return rc;
+  }
   if (gemm_use_pair(args.M)) return gemm_launch_pair(plan.map_a, plan.map_b2, epi, args, stream, &plan.map_b3);
   return gemm_launch(plan.map_a, plan.map_b, epi, args, stream);
 }

@@ -55,6 +55,8 @@ struct GemmArgs {
 };
 
 struct GemmPlan {
+  const void* A;       // activation base and leading dimension (the swap-AB kernel builds its own map over it)
+  long long lda;
   CUtensorMap map_a;
   CUtensorMap map_b;   // 256-row boxes (1-CTA kernel)
   CUtensorMap map_b2;  // 128-row boxes (2-CTA pair kernel, 256 x 256 tiles)
@@ -68,6 +70,8 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64
 // 3-D map (d0 innermost, 128B swizzle), e.g. the prefix pool [slot*layer][block_tokens][kv_dim].
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                       uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
+int make_tmap_store_3d(CUtensorMap* map, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,
+                       uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1);
 int gemm_plan(GemmPlan* plan, const void* A, long long lda, const void* B, long long ldb, int M, int N, int K);
 int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& args, cudaStream_t stream);
 // A/B maps built once (weights at init, activation buffers at init with their max rows).
@@ -78,6 +82,12 @@ size_t gemm_split_ws_bytes(int M, int N, int K);
 // 2-CTA pair variant (M > 128): map_b2 must be built with 128-row boxes (make_tmap_a on the weight).
 int gemm_launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, int epi, const GemmArgs& args,
                      cudaStream_t stream, const CUtensorMap* map_b3 = nullptr);
+// Swap-AB pair kernel for M <= 256 (gemm_swap.cu): the weight is the MMA's M operand. Returns 1 when the launch is
+// not covered (epilogue needs the row-major layout and no split-K applies); the caller then runs gemm_launch_pair /
+// gemm_launch. map_w: 128-row boxes over the weight (map_b2). x / ldx: the activation buffer.
+int gemm_launch_swap(const CUtensorMap& map_w, const void* x, long long ldx, int epi, const GemmArgs& args,
+                     cudaStream_t stream);
+bool gemm_swap_enabled();
 int make_tmap_b64(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, int K);
 bool gemm_use_pair(int M);  // pair kernel for M > 128 unless PO_GEMM_1CTA=1

@@ -178,3 +178,40 @@ def test_splitk_qkv_rope():
     rot = torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
     ref = torch.cat([rot[:, :rope_cols // hd], y[:, rope_cols // hd:]], dim=1).reshape(M, N)
     assert _rel(out, ref) < TOL_BF16
+
+
+# ---- short launches (M <= 256): swap-AB pair kernel, the weight as the MMA's M operand (csrc/gemm_swap.cu)
+@pytest.mark.parametrize("M", [1, 8, 16, 17, 100, 128, 129, 160, 255, 256])
+def test_swap_ab_unsplit_bf16_f32_silu(M):
+    """K = 512 (8 k-blocks) never splits: the transposed epilogues store straight from TMEM."""
+    torch.manual_seed(100 + M)
+    K = 512
+    A = _rand(M, K)
+    B = _rand(1024, K, scale=K ** -0.5)
+    ref = A.float() @ B.float().T
+    out = torch.empty(M, 1024, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, B, out)
+    assert _rel(out, ref) < TOL_BF16
+    out32 = torch.empty(M, 1024, dtype=torch.float32, device="cuda")
+    _gemm(A, B, out32, epi=_lib.EPI_F32)
+    assert _rel(out32, ref) < TOL_F32
+    I = 512
+    gate, up = _rand(I, K, scale=K ** -0.5), _rand(I, K, scale=K ** -0.5)
+    W = torch.stack([gate.view(I // 16, 16, K), up.view(I // 16, 16, K)], dim=1).reshape(2 * I, K).contiguous()
+    act = torch.empty(M, I, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, W, act, epi=_lib.EPI_SILU_MUL)
+    g, u = A.float() @ gate.float().T, A.float() @ up.float().T
+    assert _rel(act, g / (1 + torch.exp(-g)) * u) < TOL_BF16
+
+
+@pytest.mark.parametrize("M", [1, 33, 160, 256])
+def test_swap_ab_strided_output_rows(M):
+    """Output with a leading dimension wider than N (the engine's qkv / act rows): only [:, :N] is written."""
+    torch.manual_seed(7 + M)
+    K = 256
+    A = _rand(M, K)
+    B = _rand(512, K, scale=K ** -0.5)
+    big = torch.full((M, 768), 7.0, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, B, big[:, :512])
+    assert _rel(big[:, :512], A.float() @ B.float().T) < TOL_BF16
+    assert (big[:, 512:] == 7.0).all()
