@@ -33,7 +33,9 @@ __device__ __forceinline__ void add_parts(const PartSrc& ps, int row, int c, uin
   }
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// silu(g) = g / (1 + e^-g) with the fast division (MUFU reciprocal, no IEEE slow-path branch per element, so the
+// epilogues interleave elements); for g < -87 the denominator overflows and the result is the limit -0.
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // 1/rms of output row `row` from the producer's per-segment sums of squares (fixed summation order; the loads go
 // out 8 at a time so their latency is paid once per 8 segments, not once per segment)

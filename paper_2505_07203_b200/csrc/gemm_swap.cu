@@ -21,16 +21,20 @@ namespace po {
 
 #ifdef SWAP_TRACE
 // globaltimer stamps per CTA (tools/dbg_swap_trace.py): 0 start, 1 after setup, 2 first full barrier seen by the MMA
-// thread, 3 last MMA commit, 4 epilogue start (first tfull), 5 epilogue done, 6 exit
-__device__ unsigned long long g_swap_trace[296 * 8];
+// thread, 3 last MMA commit, 4 epilogue start (first tfull), 5 epilogue done, 6 exit, 7 last unit's epilogue start
+__device__ unsigned long long g_swap_trace[296 * 16];
 __device__ __forceinline__ unsigned long long gtime_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#ifndef SWAP_TRACE_N
+#define SWAP_TRACE_N 0
+#endif
 #define STAMP(i, cond) \
   do {                 \
-    if (cond) g_swap_trace[blockIdx.x * 8 + (i)] = gtime_ns(); \
+    if ((cond) && (SWAP_TRACE_N == 0 || (args.N == SWAP_TRACE_N && args.M > 1))) \
+      g_swap_trace[blockIdx.x * 16 + (i)] = gtime_ns(); \
   } while (0)
 #else
 #define STAMP(i, cond) \
@@ -53,7 +57,7 @@ constexpr int ACC_STRIDE = 256;  // TMEM columns between the two accumulators
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     gemm2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                  const __grid_constant__ CUtensorMap map_ws, const GemmArgs args, int np) {
+                  const __grid_constant__ CUtensorMap map_st, const GemmArgs args, int np) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sW = smem;
@@ -191,6 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
       STAMP(4, et == 0 && it == 0);
+      STAMP(7, et == 0);
       const int col = nb * 256 + (int)rank * 128 + wq * 32 + lane;  // this thread's output column
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * ACC_STRIDE;
 #pragma unroll 1
@@ -198,47 +203,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         uint32_t r[32];
         tmem_ld32(taddr + c0, r);
         tmem_ld_wait();
-        const int nr = min(32, args.M - c0);
-        if (ksp > 1) {
-          // fp32 partial [split][row][col]: stage this warp's 32 rows x 32 columns in shared memory (row-major, one
-          // 128-byte row per activation row) and write the box with one TMA store (rows >= M are clipped)
-          uint8_t* wb = stg + (wq * 2 + (nst & 1)) * 4096;
-          if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer (two boxes ago) is done
-          __syncwarp();
+        // Every mode stages this warp's 32 activation rows x 32 output columns in shared memory (row-major, one row
+        // per activation row) and writes the box with one TMA store; rows >= M are clipped by the map's bounds.
+        //   split-K: fp32 partial [split][row][col] (map_st over the workspace); F32 / BF16: the output;
+        //   SiLU.mul: 16 bf16 output columns per warp
+        uint8_t* wb = stg + (wq * 2 + (nst & 1)) * 4096;
+        STAMP(8 + 4 * (c0 / 32), et == 0 && u + npairs >= num_units && c0 < 64);
+        if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer (two boxes ago) is done
+        __syncwarp();
+        STAMP(9 + 4 * (c0 / 32), et == 0 && u + npairs >= num_units && c0 < 64);
+        int sc0 = col - lane;
+        if (ksp > 1 || EPI == EPI_F32) {
           float* t = reinterpret_cast<float*>(wb);
 #pragma unroll
           for (int j = 0; j < 32; ++j) t[j * 32 + lane] = __uint_as_float(r[j]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&map_ws, wb, col - lane, c0, u % ksp);
-            bulk_commit();
-          }
-          ++nst;
         } else if constexpr (EPI == EPI_BF16) {
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.out) + (long long)c0 * args.ldo + col;
+          __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(wb);
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nr) dst[(long long)j * args.ldo] = __float2bfloat16_rn(__uint_as_float(r[j]));
-        } else if constexpr (EPI == EPI_F32) {
-          float* dst = static_cast<float*>(args.out) + (long long)c0 * args.ldo + col;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nr) dst[(long long)j * args.ldo] = __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j) t[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
         } else if constexpr (EPI == EPI_SILU_MUL) {
           // weight rows come in 16-row groups [gate 16 | up 16]: lanes 0..15 hold gate columns, 16..31 the matching
           // up columns; output column (col / 32) * 16 + col % 32 (the row-major epilogue's interleave)
-          const int oc = (col / 32) * 16 + (col & 31);
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.out) + (long long)c0 * args.ldo + oc;
+          // Two activation rows per step with every lane busy: lanes 0..15 finish row j (own gate, partner's up),
+          // lanes 16..31 row j + 1 (partner's gate, own up); one shuffle per pair of rows, no divergence.
+          __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(wb);
+          const bool hi = lane >= 16;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float up = __shfl_down_sync(0xffffffffu, __uint_as_float(r[j]), 16);
-            if (j < nr && lane < 16) {
-              const float sc = s_inv[c0 + j];
-              dst[(long long)j * args.ldo] = __float2bfloat16_rn(silu_f(sc * __uint_as_float(r[j])) * (sc * up));
-            }
+          for (int j = 0; j < 32; j += 2) {
+            const float mine = __uint_as_float(hi ? r[j] : r[j + 1]);
+            const float other = __shfl_xor_sync(0xffffffffu, mine, 16);
+            const float g = hi ? other : __uint_as_float(r[j]);
+            const float up = hi ? __uint_as_float(r[j + 1]) : other;
+            const int row = j + (hi ? 1 : 0);
+            const float sc = s_inv[min(c0 + row, 255)];
+            t[row * 16 + (lane & 15)] = __float2bfloat16_rn(silu_f(sc * g) * (sc * up));
           }
+          sc0 /= 2;
         }
+        STAMP(10 + 4 * (c0 / 32), et == 0 && u + npairs >= num_units && c0 < 64);
+        fence_proxy_async_smem();
+        __syncwarp();
+        STAMP(11 + 4 * (c0 / 32), et == 0 && u + npairs >= num_units && c0 < 64);
+#ifndef SWAP_NO_TMA_STORE
+        if (lane == 0) {
+          tma_store_3d(&map_st, wb, sc0, c0, ksp > 1 ? u % ksp : 0);
+          bulk_commit();
+        }
+#endif
+        STAMP(14, et == 0 && u + npairs >= num_units && c0 == 0);
+        ++nst;
       }
       tc_fence_before();
       named_bar_sync(1, 128);
@@ -280,6 +293,11 @@ int splitk_reduce_launch(int epi, const GemmArgs& args, cudaStream_t stream);
 // Returns 0, a negative error, or 1 when this launch is not covered (the caller runs the row-major kernels).
 // map_w: the weight with 128-row boxes (the pair kernel's map_b2). x / ldx: the activation buffer (rows a_row0 ..
 // a_row0 + M - 1 are read; the map is bounded there, so the rounding rows of NP are zero-filled by TMA).
+#ifdef SWAP_NO_PDL
+#define PO_SWAP_LAUNCH(k, g, b, sm, st, ...) k<<<g, b, sm, st>>>(__VA_ARGS__)
+#else
+#define PO_SWAP_LAUNCH(k, g, b, sm, st, ...) launch_pdl(k, g, b, sm, st, __VA_ARGS__)
+#endif
 int gemm_launch_swap(const CUtensorMap& map_w, const void* x, long long ldx, int epi, const GemmArgs& in,
                      cudaStream_t stream) {
   GemmArgs args = in;
@@ -298,20 +316,30 @@ int gemm_launch_swap(const CUtensorMap& map_w, const void* x, long long ldx, int
     }
   }
   if (!gemm_swap_supported(epi, args.M, args.N, args.K, args.k_splits > 1)) return 1;  // not handled: caller falls back
-  CUtensorMap map_x, map_ws;
+  CUtensorMap map_x, map_st;
   if (make_tmap_2d_bf16(&map_x, x, args.K, (uint64_t)args.a_row0 + args.M, ldx * 2, BK, np / 2)) return -2;
-  std::memset(&map_ws, 0, sizeof(map_ws));
-  if (args.k_splits > 1 &&
-      make_tmap_store_3d(&map_ws, args.split_ws, true, args.N, args.M, args.k_splits, (uint64_t)args.N * 4,
-                         (uint64_t)args.N * args.M * 4, 32, 32))
-    return -2;
+  // the epilogue's TMA-store map: split-K partials [split][M][N] fp32, or the output [M][N] (row stride ldo)
+  int mrc;
+  if (args.k_splits > 1)
+    mrc = make_tmap_store_3d(&map_st, args.split_ws, true, args.N, args.M, args.k_splits, (uint64_t)args.N * 4,
+                             (uint64_t)args.N * args.M * 4, 32, 32);
+  else if (epi == EPI_F32)
+    mrc = make_tmap_store_3d(&map_st, args.out, true, args.N, args.M, 1, (uint64_t)args.ldo * 4,
+                             (uint64_t)args.ldo * 4 * args.M, 32, 32);
+  else if (epi == EPI_BF16)
+    mrc = make_tmap_store_3d(&map_st, args.out, false, args.N, args.M, 1, (uint64_t)args.ldo * 2,
+                             (uint64_t)args.ldo * 2 * args.M, 32, 32);
+  else
+    mrc = make_tmap_store_3d(&map_st, args.out, false, args.N / 2, args.M, 1, (uint64_t)args.ldo * 2,
+                             (uint64_t)args.ldo * 2 * args.M, 16, 32);
+  if (mrc) return 1;  // output not TMA-addressable (alignment): row-major kernels
   const int units = tiles * args.k_splits;
   const int np_pairs = units < pairs ? units : pairs;
   switch (epi) {
 #define PO_SWAP_CASE(E)                                                                                  \
   case E:                                                                                                \
     ensure_smem_attr<gemm2s_kernel<E>>(SMEM);                                                            \
-    launch_pdl(gemm2s_kernel<E>, dim3(2 * np_pairs), dim3(NT), SMEM, stream, map_w, map_x, map_ws, args, np);  \
+    PO_SWAP_LAUNCH(gemm2s_kernel<E>, dim3(2 * np_pairs), dim3(NT), SMEM, stream, map_w, map_x, map_st, args, np); \
     break;
     PO_SWAP_CASE(EPI_BF16)
     PO_SWAP_CASE(EPI_F32)
@@ -329,6 +357,6 @@ int gemm_launch_swap(const CUtensorMap& map_w, const void* x, long long ldx, int
 
 #ifdef SWAP_TRACE
 extern "C" int po_debug_swap_trace(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, po::g_swap_trace, sizeof(unsigned long long) * 296 * 8) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyFromSymbol(host, po::g_swap_trace, sizeof(unsigned long long) * 296 * 16) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -22,11 +22,11 @@ for _ in range(3):
     torch.cuda.synchronize()
     _lib.call("po_op_gemm", p(A), K, p(B), K, p(out), N, None, 0, M, N, K, 0, None, 0, 0, None)
     torch.cuda.synchronize()
-buf = (ctypes.c_uint64 * (296 * 8))()
+buf = (ctypes.c_uint64 * (296 * 16))()
 lib.po_debug_swap_trace(ctypes.addressof(buf))
-arr = [list(buf[i * 8:(i + 1) * 8]) for i in range(296)]
+arr = [list(buf[i * 16:(i + 1) * 16]) for i in range(296)]
 arr = [a for a in arr if a[0]]
-names = ["start", "setup_done", "first_full", "last_commit", "epi_start", "epi_done", "exit"]
+names = ["start", "setup_done", "first_full", "last_commit", "epi_start", "epi_done", "exit", "last_epi"] + [f"c{c}_{w}" for c in range(2) for w in ("ld", "buf", "staged", "fenced")]
 t0 = min(a[0] for a in arr)
 print(f"M={M} N={N} K={K}: {len(arr)} CTAs; us after the first CTA start (min / median / max)")
 for i, nm in enumerate(names):
