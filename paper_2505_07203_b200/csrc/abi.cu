@@ -65,8 +65,18 @@ int po_op_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* out
   args.split_ws_bytes = ws;
   if (ws && cudaMallocAsync(reinterpret_cast<void**>(&args.split_ws), ws, st) != cudaSuccess)
     return po::set_error(PO_ERR_CUDA, "po_op_gemm: split-K workspace allocation failed");
+  // stream-K workspace for short launches (M <= 256): partial slots + flags, zeroed flags, epoch 1
+  if (M <= 256 && po::gemm_sk_enabled()) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&args.sk_ws), po::gemm_sk_ws_bytes(), st) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&args.sk_flags), po::gemm_sk_flag_bytes(), st) != cudaSuccess)
+      return po::set_error(PO_ERR_CUDA, "po_op_gemm: stream-K workspace allocation failed");
+    cudaMemsetAsync(args.sk_flags, 0, po::gemm_sk_flag_bytes(), st);
+    args.sk_epoch = 1;
+  }
   rc = po::gemm_run(plan, epi, args, st);
   if (args.split_ws) cudaFreeAsync(args.split_ws, st);
+  if (args.sk_ws) cudaFreeAsync(args.sk_ws, st);
+  if (args.sk_flags) cudaFreeAsync(args.sk_flags, st);
   if (rc) return po::set_error(PO_ERR_CUDA, "po_op_gemm: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return PO_OK;
 }

@@ -116,6 +116,9 @@ struct po_engine {
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
   // persistent weight-streaming kernel (prefix hits): partial tiles, fix-up flags, grid-barrier counter
+  float* sk_ws = nullptr;       // stream-K short-launch GEMMs: per-CTA partial slots and flags (gemm_sk.cu)
+  uint32_t* sk_flags = nullptr;
+  uint32_t sk_epoch = 0;
   float* stream_ws = nullptr;
   size_t stream_ws_bytes = 0;
   uint32_t* stream_flags = nullptr;
@@ -394,6 +397,12 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     }
     e->gemm_ws_bytes = gw;
     if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
+    if (!f8) {  // stream-K short-launch GEMMs
+      if (dalloc(e, &e->sk_ws, po::gemm_sk_ws_bytes(), &e->workspace_bytes) ||
+          dalloc(e, &e->sk_flags, po::gemm_sk_flag_bytes(), &e->workspace_bytes))
+        return fail(PO_ERR_CUDA, "stream-K workspace failed");
+      cudaMemsetAsync(e->sk_flags, 0, po::gemm_sk_flag_bytes(), s);
+    }
     if (!f8) {  // streaming kernel (requests of <= 256 miss rows): partials at M = 256 for the four layer GEMMs
       size_t sw = 0, nf = 0;
       const int shapes[4][2] = {{qkvc, h}, {h, ctxc}, {2 * I, h}, {h, I}};
@@ -684,6 +693,10 @@ bool bounded_a_enabled();
 int gemm(const CUtensorMap& a, const void* x, long long ldx, const CUtensorMap& b1, const CUtensorMap& b2,
          const CUtensorMap& b3, int epi, const po::GemmArgs& g, cudaStream_t s) {
   if (po::gemm_swap_enabled() && g.M <= 256) {  // short launches: weight as the MMA's M operand
+    if (g.sk_ws && po::gemm_sk_enabled()) {  // stream-K: one round, in-kernel fix-up
+      const int rc = po::gemm_launch_sk(b2, x, ldx, epi, g, s);
+      if (rc != 1) return rc;
+    }
     const int rc = po::gemm_launch_swap(b2, x, ldx, epi, g, s);
     if (rc != 1) return rc;
   }
@@ -822,8 +835,13 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       return ++sa.nph == po::STREAM_MAX_PHASES ? flush() : 0;
     }
     mark(cls, true);
+    po::GemmArgs gk = g;
+    // stream-K for short requests (every layer GEMM a weight stream: prefix hits, short prompts); a long request's
+    // short launches (MLP chunk tails, the last layer's final row) keep the split-K kernels, so a result does not
+    // depend on the MLP chunk size
+    if (n_miss <= 256) { gk.sk_ws = e->sk_ws; gk.sk_flags = e->sk_flags; gk.sk_epoch = ++e->sk_epoch; }
     int r = f8 ? gemm8(a8, static_cast<const __nv_bfloat16*>(x), ldx, x8, xs, bq, bsc, epi, g, s)
-               : gemm(amap, x, ldx, b1, b2, b3, epi, g, s);
+               : gemm(amap, x, ldx, b1, b2, b3, epi, gk, s);
     mark(cls, false);
     launches += f8 ? 2 : 1;
     return r;

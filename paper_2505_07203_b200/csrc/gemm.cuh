@@ -52,6 +52,11 @@ struct GemmArgs {
   // (per-row activation scale from quantize_rows_e4m3, per-output-channel weight scale) before the epilogue.
   const float* a_scale;
   const float* b_scale;
+  // Stream-K swap-AB kernel (gemm_sk.cu, M <= 256): fp32 partial slots [num_sms][2][256][128] and one flag per slot
+  // (128-byte stride); a launch raises its dump flags to sk_epoch, which must grow from launch to launch.
+  float* sk_ws;
+  uint32_t* sk_flags;
+  uint32_t sk_epoch;
 };
 
 struct GemmPlan {
@@ -88,6 +93,15 @@ int gemm_launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, int ep
 int gemm_launch_swap(const CUtensorMap& map_w, const void* x, long long ldx, int epi, const GemmArgs& args,
                      cudaStream_t stream);
 bool gemm_swap_enabled();
+// Stream-K swap-AB kernel (gemm_sk.cu): every SM pair streams an equal share of the weight's (tile, k-block) work;
+// tiles cut between pairs are fixed up in-kernel (no reduce launch). Needs args.sk_ws / sk_flags; returns 1 when the
+// launch is not covered.
+int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int epi, const GemmArgs& args,
+                   cudaStream_t stream);
+bool gemm_sk_enabled();
+constexpr int SK_FLAG_STRIDE = 32;  // uint32 per flag line
+size_t gemm_sk_ws_bytes();          // partial slots for every CTA of a launch
+size_t gemm_sk_flag_bytes();
 int make_tmap_b64(CUtensorMap* map, const void* B, long long ldb, int N, int K);
 int make_tmap_a(CUtensorMap* map, const void* A, long long lda, long long rows, int K);
 bool gemm_use_pair(int M);  // pair kernel for M > 128 unless PO_GEMM_1CTA=1

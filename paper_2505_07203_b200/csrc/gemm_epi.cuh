@@ -367,4 +367,75 @@ __device__ __forceinline__ void splitk_reduce_quad(const GemmArgs& a, int row, i
   }
 }
 
+// ---- cross-CTA flags (stream-K fix-ups): relaxed poll, release store, generic <-> async proxy ordering
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// generic-proxy writes of other CTAs (epilogue stores) -> this CTA's async-proxy reads (TMA), and the reverse
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Fused epilogue of one 4-column group of a fixed-up (summed) row: acc = columns col..col+3; part = the partner group
+// (gate -> up at col + 16; RoPE x1 -> x2 at col + 64); sc = the row's 1/rms (folded RMSNorm consumers); rv = the
+// residual row's values (EPI_RESID_F32). Same arithmetic order as epilogue_tile / splitk_reduce_quad.
+template <int EPI>
+__device__ __forceinline__ void quad_epi(const GemmArgs& a, int row, int col, float4 acc, float4 part, float sc,
+                                         float4 rv) {
+  if constexpr (EPI == EPI_BF16) {
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col) =
+        make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    rv.x += acc.x; rv.y += acc.y; rv.z += acc.z; rv.w += acc.w;
+    *reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col) = rv;
+    if (a.xg_out) {
+      const float4 gm = *reinterpret_cast<const float4*>(a.g_next + col);
+      *reinterpret_cast<uint2*>(a.xg_out + (long long)row * a.ldxg + col) =
+          make_uint2(pack_bf16(rv.x * gm.x, rv.y * gm.y), pack_bf16(rv.z * gm.z, rv.w * gm.w));
+      float sq = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z + rv.w * rv.w;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if ((threadIdx.x & 31) == 0) a.ss_out[(long long)row * a.ss_nseg + col / 128] = sq;
+    }
+  } else if constexpr (EPI == EPI_SILU_MUL) {
+    const int oc = (col / 32) * 16 + (col % 32);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + oc) =
+        make_uint2(pack_bf16(silu_f(sc * acc.x) * (sc * part.x), silu_f(sc * acc.y) * (sc * part.y)),
+                   pack_bf16(silu_f(sc * acc.z) * (sc * part.z), silu_f(sc * acc.w) * (sc * part.w)));
+  } else if constexpr (EPI == EPI_QKV_ROPE) {
+    const int head_col = col % 128;
+    acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+    if (a.bias) {
+      acc.x += a.bias[col]; acc.y += a.bias[col + 1]; acc.z += a.bias[col + 2]; acc.w += a.bias[col + 3];
+    }
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col;
+    if (col < a.rope_cols) {
+      float4 x2 = part;
+      x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
+      if (a.bias) {
+        x2.x += a.bias[col + 64]; x2.y += a.bias[col + 65]; x2.z += a.bias[col + 66]; x2.w += a.bias[col + 67];
+      }
+      const float2* cs = a.rope + (long long)(a.pos_offset + row) * 64 + head_col;
+      const float2 c0 = cs[0], c1 = cs[1], c2 = cs[2], c3 = cs[3];
+      const uint2 lo = make_uint2(pack_bf16(acc.x * c0.x - x2.x * c0.y, acc.y * c1.x - x2.y * c1.y),
+                                  pack_bf16(acc.z * c2.x - x2.z * c2.y, acc.w * c3.x - x2.w * c3.y));
+      const uint2 hi = make_uint2(pack_bf16(x2.x * c0.x + acc.x * c0.y, x2.y * c1.x + acc.y * c1.y),
+                                  pack_bf16(x2.z * c2.x + acc.z * c2.y, x2.w * c3.x + acc.w * c3.y));
+      *reinterpret_cast<uint2*>(o) = lo;
+      *reinterpret_cast<uint2*>(o + 64) = hi;
+      if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) {
+        *reinterpret_cast<uint2*>(prow + col) = lo;
+        *reinterpret_cast<uint2*>(prow + col + 64) = hi;
+      }
+    } else {
+      const uint2 v = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+      *reinterpret_cast<uint2*>(o) = v;
+      if (__nv_bfloat16* prow = pool_row(a, row, col - head_col)) *reinterpret_cast<uint2*>(prow + col) = v;
+    }
+  }
+}
+
 }  // namespace po

@@ -1,0 +1,563 @@
+// Stream-K swap-AB pair GEMM for short launches (M <= 256 rows: prefix-hit suffixes, short requests, the last
+// layer's final row). D[M,N] = X[M,K] . W[N,K]^T with the weight as the MMA's M operand (256 weight rows per pair
+// tile, 128 per CTA) and the M activation rows as its N operand (NP = M rounded up to 16), as in gemm_swap.cu.
+//
+// Such a launch is a weight stream: its time is the weight bytes over the HBM rate the busy SMs can pull
+// (tools/probe/stream_bw.cu: ~96 KB in flight per SM needs >= 128 SMs for 6 TB/s). The per-GEMM swap kernel hands
+// whole (tile, k split) units to the pairs, so at M = 160 a Llama-3.1-8B gate/up (112 tiles) runs two rounds on 74
+// pairs with the second one half empty, and the split GEMMs pay a reduce launch each (8-13 us). Here the T x nk
+// (tile, k-block) work items are cut into one equal contiguous range per pair, so every SM streams the same weight
+// bytes in one round, and a tile cut between pairs is fixed up inside the kernel, cooperatively:
+//   * a segment covering a whole tile (gate/up) runs the fused epilogue straight from TMEM;
+//   * a CUT segment (a tile shared by pairs q0..q1) dumps its fp32 accumulator to the CTA's slot of sk_ws
+//     ([M][128] fp32, bulk stores; one slot for the pair's first segment, one for its last) and raises the slot's
+//     flag to the launch epoch. A pair's cut segments are its first and/or its last, so the dumps of a tile's
+//     contributors are all written by the time the contributors finish their ranges, which balanced ranges make
+//     simultaneous;
+//   * then each contributor j of a cut tile finalises rows [j M / c, (j + 1) M / c) of it (c contributors): one
+//     bulk copy per contributor of those rows into the freed stage ring, the sum in k order (contributor order),
+//     and the fused epilogue. The fix-up is parallel over the tile's SMs and costs one L2 round trip.
+// Flag waits go to CTAs that are resident (all CTAs are resident before any dependent launch, PDL), so they cannot
+// deadlock.
+//
+// Epilogue: the accumulator (TMEM lane = output column, TMEM column = activation row) is staged 32 rows at a time in
+// shared memory as [row][128 columns] fp32, and quad_epi (gemm_epi.cuh, the reduce kernel's arithmetic) writes every
+// mode from there: RoPE + prefix-pool admission, residual + folded-norm outputs, SiLU.mul, bf16, fp32.
+//
+// CTA pair layout (cluster of 2, 256 threads per CTA, one CTA per SM):
+//   warp 0      TMA producer (one lane): per k-block its 128 weight rows (16 KB) + NP/2 activation rows
+//   warp 1      MMA issuer (leader CTA): M256 x NP x K16 x 4 per k-block into a TMEM accumulator (double buffered)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue (thread = one of the CTA's 128 output columns while draining TMEM)
+#include "gemm.cuh"
+#include "gemm_epi.cuh"
+#include "stream.cuh"
+#include <cstdlib>
+
+namespace po {
+
+#ifdef SK_ITER_TRACE
+__device__ long long g_sk_iter[64];
+#endif
+#ifdef SK_TRACE
+// globaltimer stamps per CTA of the last launch with N == SK_TRACE_N (tools/dbg_sk_trace.py): 0 start, 1 setup done,
+// 2 first full barrier (MMA), 3 last MMA commit, 4 first tfull (epilogue), 5 a dump published, 6 fix-up flags seen,
+// 7 fix-up rows landed, 8 epilogue done, 9 exit
+__device__ unsigned long long g_sk_trace[296 * 16];
+__device__ __forceinline__ unsigned long long sk_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SKT(i, cond) \
+  do {               \
+    if ((cond) && args.N == SK_TRACE_N && args.M > 1) g_sk_trace[blockIdx.x * 16 + (i)] = sk_gtime(); \
+  } while (0)
+#else
+#define SKT(i, cond) \
+  do {               \
+  } while (0)
+#endif
+
+namespace {
+constexpr int BK = 64;
+constexpr int W_BYTES = 128 * BK * 2;  // 16 KB: this CTA's 128 weight rows of a k-block
+constexpr int X_MAX = 128 * BK * 2;    // up to 128 activation rows (NP <= 256, half per CTA)
+constexpr int STAGE = W_BYTES + X_MAX;
+constexpr int STAGES = 6;
+constexpr int CH = 32;                   // activation rows per epilogue chunk
+constexpr int CH_BYTES = CH * 128 * 4;   // one chunk of the CTA's 128 columns in fp32 (= W_BYTES: a fix-up piece)
+constexpr int SMEM = STAGES * STAGE + 2 * CH_BYTES + 1024 + 256 + 1024;
+constexpr int NT = 256;
+constexpr int ACC_STRIDE = 256;          // TMEM columns between the two accumulators
+}  // namespace
+
+// Segment of a pair's range [f, hi) that starts at work item f: tile t, k-blocks [a, b).
+struct SkSeg {
+  int t, a, b;
+};
+__device__ __forceinline__ SkSeg sk_seg(int f, int hi, int nk) {
+  SkSeg s;
+  s.t = f / nk;
+  s.a = f - s.t * nk;
+  s.b = min(nk, hi - s.t * nk);
+  return s;
+}
+
+// Per-column constants of the row-major epilogue for this thread's 4 columns [col, col + 4) of a 128-column half tile
+struct SkCols {
+  float4 g4, b1, b2;
+};
+template <int EPI>
+__device__ __forceinline__ SkCols sk_cols(const GemmArgs& a, int col, int lc) {
+  SkCols k{};
+  if (EPI == EPI_RESID_F32 && a.xg_out) k.g4 = *reinterpret_cast<const float4*>(a.g_next + col);
+  if (EPI == EPI_QKV_ROPE && a.bias) {
+    k.b1 = *reinterpret_cast<const float4*>(a.bias + col);
+    if (col < a.rope_cols && lc < 64) k.b2 = *reinterpret_cast<const float4*>(a.bias + col + 64);
+  }
+  return k;
+}
+
+// Fused epilogue of rows row0 + i (i < nrows; warp wq takes i = wq, wq + 4, ...) of a CTA's 128-column half tile,
+// row-major: lane = 4 columns [col, col + 4) (lc = col - col0). src(i, off) returns the summed fp32 values of local
+// row i at columns lc + off .. + 3. aux: per local row, the residual values of the half tile (EPI_RESID_F32, 128
+// floats) or the RoPE (cos, sin) pairs of the row's position (EPI_QKV_ROPE, 64 float2), aux_ld floats apart; shared
+// memory (fix-up: bulk-copied next to the partials, so the loop issues no global load) or global memory. slots:
+// the prefix-pool slot of each local row's block (admission; shared memory) or null (read kv_slot). One warp per
+// SM sub-partition runs this, so a row's dependent chain (shared loads, MUFU, store) is exposed unless independent
+// rows overlap: unrolled by 4 (a single-row loop measured ~675 cycles per row). Arithmetic as quad_epi's.
+template <int EPI, typename Src>
+__device__ __forceinline__ void sk_rows(const GemmArgs& a, int row0, int nrows, int wq, int lane, int col0,
+                                        const float* s_inv, const SkCols& kc, const float* aux, int aux_ld,
+                                        const int* slots, Src src) {
+  const int lc = lane * 4;
+  const int col = col0 + lc;
+#ifdef SK_ITER_TRACE
+  long long t_beg = clock64(), t_prev = t_beg, d_max = 0, d_first = -1;
+#endif
+#pragma unroll 4
+  for (int i = wq; i < nrows; i += 4) {
+#ifdef SK_ITER_TRACE
+    {
+      const long long t = clock64();
+      if (i > wq) { d_max = max(d_max, t - t_prev); if (d_first < 0) d_first = t - t_prev; }
+      t_prev = t;
+    }
+#endif
+    const int row = row0 + i;
+    if constexpr (EPI == EPI_RESID_F32) {
+      const float4 a4 = src(i, 0);
+      float4 v = *reinterpret_cast<const float4*>(aux + (long long)i * aux_ld + lc);
+      v.x += a4.x; v.y += a4.y; v.z += a4.z; v.w += a4.w;
+      *reinterpret_cast<float4*>(a.resid + (long long)row * a.ldr + col) = v;
+      if (a.xg_out) {
+        *reinterpret_cast<uint2*>(a.xg_out + (long long)row * a.ldxg + col) =
+            make_uint2(pack_bf16(v.x * kc.g4.x, v.y * kc.g4.y), pack_bf16(v.z * kc.g4.z, v.w * kc.g4.w));
+        float sq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) a.ss_out[(long long)row * a.ss_nseg + col / 128] = sq;
+      }
+    } else if constexpr (EPI == EPI_QKV_ROPE) {
+      const bool rot = col < a.rope_cols;
+      if (rot && lc >= 64) continue;  // the partner lane (lc - 64) writes the rotated pair
+      const int pos = a.pos_offset + row;
+      int pslot = -1;
+      if (a.kv_pool && col0 >= a.kv_col0) pslot = slots ? slots[i] : a.kv_slot[pos >> 4];
+      __nv_bfloat16* prow = pslot >= 0
+          ? a.kv_pool + (((long long)pslot * a.pool_layers + a.pool_layer) * 16 + (pos & 15)) * a.kv_dim - a.kv_col0
+          : nullptr;
+      const float sc = s_inv[row];
+      float4 acc = src(i, 0);
+      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+      acc.x += kc.b1.x; acc.y += kc.b1.y; acc.z += kc.b1.z; acc.w += kc.b1.w;
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (long long)row * a.ldo + col;
+      if (rot) {
+        float4 x2 = src(i, 64);
+        x2.x *= sc; x2.y *= sc; x2.z *= sc; x2.w *= sc;
+        x2.x += kc.b2.x; x2.y += kc.b2.y; x2.z += kc.b2.z; x2.w += kc.b2.w;
+        const float4 ca = *reinterpret_cast<const float4*>(aux + (long long)i * aux_ld + 2 * lc);
+        const float4 cb = *reinterpret_cast<const float4*>(aux + (long long)i * aux_ld + 2 * lc + 4);
+        const uint2 lo = make_uint2(pack_bf16(acc.x * ca.x - x2.x * ca.y, acc.y * ca.z - x2.y * ca.w),
+                                    pack_bf16(acc.z * cb.x - x2.z * cb.y, acc.w * cb.z - x2.w * cb.w));
+        const uint2 hi = make_uint2(pack_bf16(x2.x * ca.x + acc.x * ca.y, x2.y * ca.z + acc.y * ca.w),
+                                    pack_bf16(x2.z * cb.x + acc.z * cb.y, x2.w * cb.z + acc.w * cb.w));
+        *reinterpret_cast<uint2*>(o) = lo;
+        *reinterpret_cast<uint2*>(o + 64) = hi;
+        if (prow) {
+          *reinterpret_cast<uint2*>(prow + col) = lo;
+          *reinterpret_cast<uint2*>(prow + col + 64) = hi;
+        }
+      } else {
+        const uint2 v = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+        *reinterpret_cast<uint2*>(o) = v;
+        if (prow) *reinterpret_cast<uint2*>(prow + col) = v;
+      }
+    } else if constexpr (EPI == EPI_SILU_MUL) {
+#ifdef SK_NOSTORE
+      {
+        const float4 u = src(i, 0), w2 = src(i, 16);
+        if (u.x + w2.y == 12345.f) *static_cast<float*>(a.out) = u.z;
+      }
+#else
+      if ((lc & 31) < 16) quad_epi<EPI>(a, row, col, src(i, 0), src(i, 16), s_inv[row], float4{});
+#endif
+    } else if constexpr (EPI == EPI_F32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(a.out) + (long long)row * a.ldo + col) = src(i, 0);
+    } else {
+      quad_epi<EPI>(a, row, col, src(i, 0), float4{}, 1.f, float4{});
+    }
+  }
+#ifdef SK_ITER_TRACE
+  if (blockIdx.x < 4 && (threadIdx.x & 31) == 0 && a.N == 28672 && a.M > 1)
+    printf("blk %d warp %d rows %d: total %lld first %lld max %lld\n", blockIdx.x, threadIdx.x / 32, nrows,
+           clock64() - t_beg, d_first, d_max);
+#endif
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    gemm_sk_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                   const GemmArgs args, int np) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + STAGES * W_BYTES;
+  uint8_t* stg = smem + STAGES * STAGE;
+  float* s_inv = reinterpret_cast<float*>(stg + 2 * CH_BYTES);  // 1/rms per activation row (<= 256)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + 2 * CH_BYTES + 1024);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* fx_bar = tempty_bar + 2;  // fix-up copies, one phase per cut tile
+  uint64_t* ss_bar = fx_bar + 1;      // the rows' RMS segment sums (folded-norm consumers)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ss_bar + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int P = gridDim.x >> 1;
+  const int nk = args.K / BK;
+  const long long W = (long long)(args.N / 256) * nk;
+  const int lo = stream_pair_start(W, P, pair);
+  const int hi = stream_pair_start(W, P, pair + 1);
+  const int M = args.M;
+  const int xh = np / 2;
+  const uint32_t x_bytes = (uint32_t)xh * BK * 2;
+  SKT(0, threadIdx.x == 0);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_w);
+    tma_prefetch_desc(&map_x);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2);
+    }
+    mbar_init(fx_bar, 1);
+    mbar_init(ss_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  SKT(1, threadIdx.x == 0);
+  // weights are constant: the producer streams its first STAGES weight k-blocks before waiting for the kernel that
+  // writes the activations
+  if (warp != 0) pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int pend_s[STAGES], pend_kb[STAGES];
+      int npend = 0;
+      bool open = false;
+      const int xrow = args.a_row0 + (int)rank * xh;
+      auto flush = [&]() {
+        pdl_wait();
+        open = true;
+        for (int i = 0; i < npend; ++i)
+          tma_load_2d_pair(sX + pend_s[i] * X_MAX, &map_x, full0 + pend_s[i] * 8, pend_kb[i] * BK, xrow);
+        npend = 0;
+      };
+      for (int f = lo; f < hi;) {
+        const SkSeg sg = sk_seg(f, hi, nk);
+        for (int kb = sg.a; kb < sg.b; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * (W_BYTES + x_bytes));
+          const uint32_t fb = full0 + s * 8;
+          tma_load_2d_pair(sW + s * W_BYTES, &map_w, fb, kb * BK, sg.t * 256 + (int)rank * 128);
+          if (open) {
+            tma_load_2d_pair(sX + s * X_MAX, &map_x, fb, kb * BK, xrow);
+          } else {
+            pend_s[npend] = s;
+            pend_kb[npend] = kb;
+            if (++npend == STAGES) flush();
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        f = sg.t * nk + sg.b;
+      }
+      if (!open) flush();
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)np);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int f = lo; f < hi; ++it) {
+        const SkSeg sg = sk_seg(f, hi, nk);
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * ACC_STRIDE;
+        for (int kb = sg.a; kb < sg.b; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          SKT(2, it == 0 && kb == sg.a);
+          const uint64_t adesc = sdesc_kmajor_sw128(smem_u32(sW + s * W_BYTES));
+          const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sX + s * X_MAX));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != sg.a || k != 0) ? 1u : 0u);
+          mma_commit_pair(&empty_bar[s], 0x3);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        mma_commit_pair(&tfull_bar[acc], 0x3);
+        f = sg.t * nk + sg.b;
+      }
+      SKT(3, true);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wq = warp & 3;
+    const int et = threadIdx.x - 128;  // this thread's column of the CTA's 128 while draining TMEM
+    const int lc = lane * 4;           // ... and its 4 columns in the row-major epilogue
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    if (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
+      // 1/rms of every activation row, once per launch: the rows' segment sums arrive by bulk copy (one L2 round
+      // trip instead of a dependent chain per row), then each thread sums its rows in segment order (row_inv_rms)
+      const int nseg = args.ss_nseg;
+      if (!args.ss_in || (reinterpret_cast<uintptr_t>(args.ss_in) & 15) || ((nseg * 4) & 15)) {
+        // (bulk copies need 16-byte aligned rows: small models / odd row offsets load per row)
+        for (int r = et; r < M; r += 128) s_inv[r] = args.ss_in ? row_inv_rms(args, r) : 1.0f;
+      } else {
+        const int rpp = min(M, (2 * CH_BYTES) / (nseg * 4));  // rows per staged piece
+        const float* ss = reinterpret_cast<const float*>(stg);
+        uint32_t ph = 0;
+        for (int p0 = 0; p0 < M; p0 += rpp, ph ^= 1) {
+          const int nr = min(rpp, M - p0);
+          if (et == 0) {
+            mbar_arrive_expect_tx(ss_bar, (uint32_t)nr * nseg * 4);
+            bulk_g2s(stg, args.ss_in + (size_t)p0 * nseg, (uint32_t)nr * nseg * 4, ss_bar);
+          }
+          mbar_wait(ss_bar, ph);
+          for (int r = et; r < nr; r += 128) {
+            float sum = 0.f;
+            for (int i = 0; i < nseg; ++i) sum += ss[r * nseg + i];
+            s_inv[p0 + r] = rsqrtf(sum / args.norm_dim + args.norm_eps);
+          }
+          named_bar_sync(1, 128);  // the next piece overwrites the staging buffer
+        }
+      }
+    }
+    const int first_t = lo / nk;
+    int it = 0, nch = 0;
+    for (int f = lo; f < hi; ++it) {
+      const SkSeg sg = sk_seg(f, hi, nk);
+      f = sg.t * nk + sg.b;
+      const bool cut = sg.a > 0 || sg.b < nk;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      SKT(4, et == 0 && it == 0);
+      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * ACC_STRIDE;
+      const int col0 = sg.t * 256 + (int)rank * 128;  // the CTA's first output column of this tile
+      const int slot = (int)blockIdx.x * 2 + (sg.t == first_t ? 0 : 1);  // dump slot of a cut segment
+      const SkCols kc = cut ? SkCols{} : sk_cols<EPI>(args, col0 + lc, lc);
+#pragma unroll 1
+      for (int c0 = 0; c0 < M; c0 += CH, ++nch) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c0, r);
+        tmem_ld_wait();
+        const int rows = min(CH, M - c0);
+        if (cut) {  // the fp32 partial, straight from registers: one 128-byte line per warp and row
+          float* dst = args.sk_ws + ((size_t)slot * 256 + c0) * 128 + et;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < rows) dst[i * 128] = __uint_as_float(r[i]);
+          continue;
+        }
+        float* buf = reinterpret_cast<float*>(stg + (nch & 1) * CH_BYTES);
+        named_bar_sync(1, 128);  // every thread's epilogue reads of this buffer (two chunks ago) are done
+#pragma unroll
+        for (int i = 0; i < 32; ++i) buf[i * 128 + et] = __uint_as_float(r[i]);
+        named_bar_sync(1, 128);
+        const float* brow = buf + lc;
+        const float* aux = EPI == EPI_RESID_F32 ? args.resid + (long long)c0 * args.ldr + col0
+                           : EPI == EPI_QKV_ROPE ? reinterpret_cast<const float*>(args.rope + (long long)(args.pos_offset + c0) * 64)
+                                                 : nullptr;
+        sk_rows<EPI>(args, c0, rows, wq, lane, col0, s_inv, kc, aux,
+                     EPI == EPI_RESID_F32 ? (int)args.ldr : 128, nullptr, [=](int i, int off) {
+                       return *reinterpret_cast<const float4*>(brow + i * 128 + off);
+                     });
+      }
+      if (cut) __threadfence();  // this thread's partial stores, before the flag below
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        mbar_arrive_cluster(tempty0 + acc * 8);
+        if (cut) {  // publish the partial
+          st_release_u32(args.sk_flags + (size_t)slot * SK_FLAG_STRIDE, args.sk_epoch);
+          SKT(5, true);
+        }
+      }
+    }
+    // Cooperative fix-up of the cut tiles this pair holds a segment of: its first and/or last segment. The stage
+    // ring is free (every MMA of this CTA has completed), so each contributor's rows of this CTA's share land there.
+    const SkSeg first = sk_seg(lo, hi, nk);
+    const SkSeg last = sk_seg(max(lo, (hi - 1) / nk * nk), hi, nk);
+    uint32_t fx_phase = 0;
+#pragma unroll 1
+    for (int w = 0; w < 2; ++w) {
+      const SkSeg sg = w == 0 ? first : last;
+      if (w == 1 && last.t == first.t) break;
+      if (sg.a == 0 && sg.b == nk) continue;  // a whole tile: done above
+      const int t = sg.t;
+      const int q0 = stream_owner(W, P, t * nk), q1 = stream_owner(W, P, t * nk + nk - 1);
+      const int c = q1 - q0 + 1, j = pair - q0;
+      const int r0 = (int)((long long)j * M / c), r1 = (int)((long long)(j + 1) * M / c);
+      if (r0 == r1) continue;
+      const int nr = r1 - r0;
+      const uint32_t bytes = (uint32_t)nr * 512;
+      float* aux = reinterpret_cast<float*>(smem + (size_t)c * bytes);  // residual or RoPE rows of the share
+      int* s_slot = reinterpret_cast<int*>(stg);                       // pool slot per row of the share (<= 128)
+      if (EPI == EPI_QKV_ROPE && args.kv_pool)
+        for (int i = et; i < nr; i += 128) s_slot[i] = args.kv_slot[(args.pos_offset + r0 + i) >> 4];
+      const int col0 = t * 256 + (int)rank * 128;
+      if (warp == 4) {
+        // poll every contributor's dump flag for this tile (slot 0 if the tile is its first segment's), one lane each
+        bool ok;
+        uint32_t ns = 32;
+        do {
+          ok = true;
+          for (int q = q0 + lane; q <= q1; q += 32) {
+            const int qs = (2 * q + (int)rank) * 2 + (stream_pair_start(W, P, q) / nk == t ? 0 : 1);
+            ok &= (int)(ld_relaxed_u32(args.sk_flags + (size_t)qs * SK_FLAG_STRIDE) - args.sk_epoch) >= 0;
+          }
+          ok = __all_sync(0xffffffffu, ok);
+#ifdef PO_DEBUG_HANG
+          if (!ok && ns == 256 && lane == 0) {
+            static_assert(true, "");
+            if (clock64() % 100000 < 50)
+              printf("SK POLL block %d tile %d q0 %d q1 %d epoch %u M %d N %d K %d\n", blockIdx.x, t, q0, q1,
+                     args.sk_epoch, M, args.N, args.K);
+          }
+#endif
+          if (!ok) {
+            __nanosleep(ns);
+            ns = ns < 256 ? ns * 2 : 256;
+          }
+        } while (!ok);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        fence_proxy_async_global();
+        SKT(6, lane == 0);
+        const uint32_t aux_bytes = (EPI == EPI_RESID_F32 || EPI == EPI_QKV_ROPE) ? bytes : 0;
+        if (lane == 0) mbar_arrive_expect_tx(fx_bar, bytes * c + aux_bytes);
+        __syncwarp();
+        for (int q = q0 + lane; q <= q1; q += 32) {
+          const int qs = (2 * q + (int)rank) * 2 + (stream_pair_start(W, P, q) / nk == t ? 0 : 1);
+          bulk_g2s(smem + (size_t)(q - q0) * bytes, args.sk_ws + ((size_t)qs * 256 + r0) * 128, bytes, fx_bar);
+        }
+        if constexpr (EPI == EPI_RESID_F32) {  // the share's residual rows (512 B each at row stride ldr)
+          for (int i = lane; i < nr; i += 32)
+            bulk_g2s(aux + i * 128, args.resid + (long long)(r0 + i) * args.ldr + col0, 512, fx_bar);
+        } else if constexpr (EPI == EPI_QKV_ROPE) {  // the positions' (cos, sin) rows: one contiguous block
+          if (lane == 0) bulk_g2s(aux, args.rope + (long long)(args.pos_offset + r0) * 64, bytes, fx_bar);
+        }
+      }
+      mbar_wait(fx_bar, fx_phase);
+      fx_phase ^= 1;
+      if (EPI == EPI_QKV_ROPE && args.kv_pool) named_bar_sync(1, 128);  // s_slot
+      SKT(7, et == 0);
+      SKT(10 + 3 * w, et == 0);
+      const SkCols kc = sk_cols<EPI>(args, col0 + lc, lc);
+      const float* part = reinterpret_cast<const float*>(smem) + lc;
+      const int pstride = (int)(bytes / 4);
+#ifdef SK_NOEPI
+      if (nr > 100000)
+#endif
+      sk_rows<EPI>(args, r0, nr, wq, lane, col0, s_inv, kc, aux, 128, s_slot, [=](int i, int off) {
+        const float* p = part + i * 128 + off;
+        float4 v = *reinterpret_cast<const float4*>(p);
+        for (int q = 1; q < c; ++q) {
+          const float4 u = *reinterpret_cast<const float4*>(p + q * pstride);
+          v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+        }
+        return v;
+      });
+      SKT(12 + 3 * w, et == 0);
+      named_bar_sync(1, 128);  // the copies of the next cut tile overwrite these rows
+    }
+    SKT(8, et == 0);
+
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+  SKT(9, threadIdx.x == 0);
+}
+
+// PO_SK=1 runs short launches through this kernel. Off by default: its mainloop streams the weights faster than the
+// per-GEMM swap kernel (gate/up 41 vs ~55 us, every SM busy in one round), but the fix-up tail (dump, flag wait,
+// per-row epilogue at ~700 cycles per row and warp) costs more than the split-K reduce launches it replaces: prefix
+// hit 7.4 vs 6.6 ms.
+bool gemm_sk_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("PO_SK");
+    on = (v && v[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+size_t gemm_sk_ws_bytes() { return (size_t)num_sms() * 2 * 256 * 128 * sizeof(float); }
+size_t gemm_sk_flag_bytes() { return (size_t)num_sms() * 2 * SK_FLAG_STRIDE * sizeof(uint32_t); }
+
+int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int epi, const GemmArgs& in,
+                   cudaStream_t stream) {
+  if (!in.sk_ws || !in.sk_flags || in.M < 1 || in.M > 256 || in.N % 256 || in.K % BK || in.K <= 0) return 1;
+  GemmArgs args = in;
+  args.k_splits = 1;
+  const int np = (args.M + 15) / 16 * 16;
+  const long long W = (long long)(args.N / 256) * (args.K / BK);
+  const int P = (int)(W < num_sms() / 2 ? W : num_sms() / 2);
+  CUtensorMap map_x;
+  if (make_tmap_2d_bf16(&map_x, x, args.K, (uint64_t)args.a_row0 + args.M, ldx * 2, BK, np / 2)) return -2;
+  switch (epi) {
+#define PO_SK_CASE(E)                                                                                  \
+  case E:                                                                                              \
+    ensure_smem_attr<gemm_sk_kernel<E>>(SMEM);                                                         \
+    launch_pdl(gemm_sk_kernel<E>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, args, np);        \
+    break;
+    PO_SK_CASE(EPI_BF16)
+    PO_SK_CASE(EPI_F32)
+    PO_SK_CASE(EPI_SILU_MUL)
+    PO_SK_CASE(EPI_RESID_F32)
+    PO_SK_CASE(EPI_QKV_ROPE)
+#undef PO_SK_CASE
+    default: return 1;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+}  // namespace po
+
+#ifdef SK_ITER_TRACE
+extern "C" int po_debug_sk_iter(long long* h) {
+  return cudaMemcpyFromSymbol(h, po::g_sk_iter, sizeof(long long) * 64) == cudaSuccess ? 0 : -1;
+}
+#endif
+#ifdef SK_TRACE
+extern "C" int po_debug_swap_trace(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, po::g_sk_trace, sizeof(unsigned long long) * 296 * 16) == cudaSuccess ? 0 : -1;
+}
+#endif
