@@ -116,6 +116,7 @@ struct po_engine {
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
   // persistent weight-streaming kernel (prefix hits): partial tiles, fix-up flags, grid-barrier counter
+  unsigned int* lm_ticket = nullptr;  // multi-CTA LM head: CTAs finished (the last one runs the softmax)
   float* sk_ws = nullptr;       // stream-K short-launch GEMMs: per-CTA partial slots and flags (gemm_sk.cu)
   uint32_t* sk_flags = nullptr;
   uint32_t sk_epoch = 0;
@@ -397,6 +398,8 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     }
     e->gemm_ws_bytes = gw;
     if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
+    if (dalloc(e, &e->lm_ticket, 4, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "LM head counter failed");
+    cudaMemsetAsync(e->lm_ticket, 0, 4, s);
     if (!f8) {  // stream-K short-launch GEMMs
       if (dalloc(e, &e->sk_ws, po::gemm_sk_ws_bytes(), &e->workspace_bytes) ||
           dalloc(e, &e->sk_flags, po::gemm_sk_flag_bytes(), &e->workspace_bytes))
@@ -894,8 +897,13 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     rc |= run_gemm(KC_O, e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go,
                    e->map_ctx8, e->ctx8, e->ctx_s, ly.f8_o, ly.s_o);
-    for (int lo = row0; lo < n_miss && !rc; lo += c.chunk) {
-      const int cr = (n_miss - lo) < c.chunk ? (n_miss - lo) : c.chunk;
+    // balanced chunks: ceil(rows / chunk) pieces of equal size (<= chunk), so no piece is a short tail whose GEMMs
+    // leave most SM pairs idle (20,000 rows at chunk 2304: nine pieces of 2,223 rows = 9 x 256-row tiles each)
+    const int mlp_rows = n_miss - row0;
+    const int n_pieces = (mlp_rows + c.chunk - 1) / c.chunk;
+    const int piece = n_pieces > 0 ? (mlp_rows + n_pieces - 1) / n_pieces : c.chunk;
+    for (int lo = row0; lo < n_miss && !rc; lo += piece) {
+      const int cr = (n_miss - lo) < piece ? (n_miss - lo) : piece;
       po::GemmArgs gu{};
       gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws; gu.split_ws_bytes = e->gemm_ws_bytes;
@@ -916,7 +924,7 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
                            cudaGetErrorString(cudaGetLastError()));
   mark(KC_LM_HEAD, true);
   po::launch_lm_head(e->resid + (size_t)(n_miss - 1) * h, h, e->final_norm, c.rms_eps, e->lm_head, d_allowed,
-                     n_allowed, d_logits, d_probs, d_argmax, s);
+                     n_allowed, d_logits, d_probs, d_argmax, e->lm_ticket, s);
   mark(KC_LM_HEAD, false);
   ++launches;
   e->last_launches = launches;

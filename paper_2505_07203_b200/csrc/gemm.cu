@@ -28,11 +28,11 @@ constexpr int GROUP_M = 16;                     // tile raster: 16 m-blocks shar
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 }  // namespace
 
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
-  const int per_group = GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& m_blk, int& n_blk, int gm = GROUP_M) {
+  const int per_group = gm * num_n;
   const int g = t / per_group;
-  const int first_m = g * GROUP_M;
-  const int gsz = min(num_m - first_m, GROUP_M);
+  const int first_m = g * gm;
+  const int gsz = min(num_m - first_m, gm);
   const int local = t - g * per_group;
   m_blk = first_m + local % gsz;
   n_blk = local / gsz;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t / ksp, num_m, num_n, mb, nb);
+        tile_coords(t / ksp, num_m, num_n, mb, nb, args.group_m > 0 ? args.group_m : GROUP_M);
         const int kb0 = (t % ksp) * kbps;
         const int nk = min(nk_total, kb0 + kbps) - kb0;
         for (int k = 0; k < nk; ++k) {
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int mb, nb;
-      tile_coords(t / ksp, num_m, num_n, mb, nb);
+      tile_coords(t / ksp, num_m, num_n, mb, nb, args.group_m > 0 ? args.group_m : GROUP_M);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_ph);
@@ -256,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
       };
       for (int t = pair; t < num_tiles; t += npairs) {
         int mb, nb;
-        tile_coords(t / ksp, num_m, num_n, mb, nb);
+        tile_coords(t / ksp, num_m, num_n, mb, nb, args.group_m > 0 ? args.group_m : GROUP_M);
         const int kb0 = (t % ksp) * kbps;
         const int nk = min(nk_total, kb0 + kbps) - kb0;
         const int arow = args.a_row0 + mb * 2 * BM + rank * BM;
@@ -321,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
     int it = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
       int mb, nb;
-      tile_coords(t / ksp, num_m, num_n, mb, nb);
+      tile_coords(t / ksp, num_m, num_n, mb, nb, args.group_m > 0 ? args.group_m : GROUP_M);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_ph);
@@ -543,9 +543,25 @@ bool gemm_pair_narrow(int M, int N) {
   return mode && M <= 2 * BM && N / BN < num_sms() / 2 && N % 128 == 0;
 }
 
+// Raster group for a pair launch: m-blocks (256 rows) per sweep over N. The group's A rows should stay in L2 while B
+// streams past them: 16 blocks of a K = 4096 operand are 32 MB, but the down projection's K = 14336 makes 16 blocks
+// 117 MB (the whole L2), and ncu showed its A re-streamed (2.8x the algorithmic reads). Long-K launches therefore
+// take PO_GROUP_LONGK blocks (default 8: 58 MB of A). The default for K <= 8192 stays 16.
+static int pair_group(int K) {
+  static int longk = -1;
+  if (longk < 0) {
+    const char* v = getenv("PO_GROUP_LONGK");
+    longk = v ? atoi(v) : 8;
+    if (longk < 1) longk = 16;
+  }
+  return K > 8192 ? longk : GROUP_M;
+}
+
 template <int EPI>
 static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, const CUtensorMap* map_b3,
-                       const GemmArgs& in, cudaStream_t stream) {
+                       const GemmArgs& in0, cudaStream_t stream) {
+  GemmArgs in = in0;
+  if (in.group_m <= 0) in.group_m = pair_group(in.K);
   if (map_b3 && gemm_pair_narrow(in.M, in.N)) return launch_pair_t<EPI, 128>(map_a, *map_b3, in, stream);
   return launch_pair_t<EPI, 256>(map_a, map_b2, in, stream);
 }

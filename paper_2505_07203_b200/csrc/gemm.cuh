@@ -57,6 +57,8 @@ struct GemmArgs {
   float* sk_ws;
   uint32_t* sk_flags;
   uint32_t sk_epoch;
+  // tile raster of the row-major kernels: m-blocks per sweep over N (0 = the launcher's choice by K)
+  int group_m;
 };
 
 struct GemmPlan {

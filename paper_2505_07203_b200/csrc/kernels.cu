@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
                                                        const __nv_bfloat16* __restrict__ w,
                                                        const int* __restrict__ allowed, int n_allowed,
                                                        float* __restrict__ logits, float* __restrict__ probs,
-                                                       int* __restrict__ argmax) {
+                                                       int* __restrict__ argmax, unsigned int* __restrict__ ticket) {
   extern __shared__ float h[];  // [hidden] normalised last-row hidden state (bf16 values)
   __shared__ float red[32];
   pdl_wait();
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
     h[k] = __bfloat162float(__float2bfloat16_rn(x[k] * inv * gamma[k]));
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int a = warp; a < n_allowed; a += nw) {
+  for (int a = blockIdx.x * nw + warp; a < n_allowed; a += gridDim.x * nw) {
     const uint4* row = reinterpret_cast<const uint4*>(w + (long long)allowed[a] * hidden);
     float acc = 0.f;
     for (int q = lane; q < hidden / 8; q += 32) {
@@ -164,6 +164,17 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) logits[a] = acc;
+  }
+  if (gridDim.x > 1) {
+    // several CTAs share the rows (long allowed lists): the last one to finish runs the softmax / argmax
+    __shared__ unsigned int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
   }
   __threadfence_block();
   __syncthreads();
@@ -201,10 +212,20 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
   for (int a = threadIdx.x; a < n_allowed; a += blockDim.x) probs[a] = expf(logits[a] - gm) / se;
   if (threadIdx.x == 0) *argmax = bidx[0];
 }
+// One CTA (32 warps, one allowed row each at a time) up to 256 rows: Yes/No lists are latency-bound and a single CTA
+// avoids the cross-CTA hand-off. Longer lists spread the rows over up to one CTA per SM (each streams its rows'
+// 8 KB at its own share of HBM), and the last CTA to finish runs the softmax / argmax; logits and probabilities are
+// the same as the single-CTA kernel's (same per-row reduction, same final CTA code).
 void launch_lm_head(const float* resid_row, int hidden, const float* gamma, float eps, const __nv_bfloat16* w,
-                    const int* allowed, int n_allowed, float* logits, float* probs, int* argmax, cudaStream_t s) {
-  launch_pdl(lm_head_kernel, dim3(1), dim3(1024), hidden * sizeof(float), s, resid_row, hidden, gamma, eps, w, allowed,
-             n_allowed, logits, probs, argmax);
+                    const int* allowed, int n_allowed, float* logits, float* probs, int* argmax, unsigned int* ticket,
+                    cudaStream_t s) {
+  int ctas = 1;
+  if (ticket && n_allowed > 256) {
+    ctas = (n_allowed + 31) / 32;
+    if (ctas > 148) ctas = 148;
+  }
+  launch_pdl(lm_head_kernel, dim3(ctas), dim3(1024), hidden * sizeof(float), s, resid_row, hidden, gamma, eps, w,
+             allowed, n_allowed, logits, probs, argmax, ticket);
 }
 
 }  // namespace po

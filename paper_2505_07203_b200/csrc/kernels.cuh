@@ -35,6 +35,7 @@ void launch_kv_gather(const __nv_bfloat16* pool, const int* slots, int n_rows, i
                       int block_tokens, int kv_dim, __nv_bfloat16* qkv, long long ld, int col0, cudaStream_t s);
 // Last-row final norm + allowed-row LM head + restricted softmax + argmax.
 void launch_lm_head(const float* resid_row, int hidden, const float* gamma, float eps, const __nv_bfloat16* w,
-                    const int* allowed, int n_allowed, float* logits, float* probs, int* argmax, cudaStream_t s);
+                    const int* allowed, int n_allowed, float* logits, float* probs, int* argmax, unsigned int* ticket,
+                    cudaStream_t s);
 
 }  // namespace po

@@ -81,6 +81,16 @@ def test_tiny_many_allowed_ids(tiny_engine):
     check_against_oracle(TINY, res, toks, allowed, 42)
 
 
+def test_tiny_whole_vocab_allowed(tiny_engine):
+    # the LM head spreads a long allowed list over many CTAs (one per SM at most) and the last one runs the softmax
+    toks = tokens_for(5, 300)
+    allowed = list(range(32000))
+    res = tiny_engine.prefill(toks, allowed)
+    check_against_oracle(TINY, res, toks, allowed, 42)
+    again = tiny_engine.prefill(toks, allowed)
+    assert np.array_equal(res.logits, again.logits) and res.index == again.index
+
+
 def test_small_gqa_chunked_mlp():
     toks = tokens_for(9, 1500)
     with Engine(SMALL, seed=7, max_tokens=2048, chunk=512, pool_blocks=64) as e:
