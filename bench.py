@@ -369,8 +369,14 @@ def executed_flops_per_class(M, n: int, last_row_only: bool) -> dict:
     L = M.num_layers
     rows = (L - 1) * n + 1 if last_row_only else L * n  # row-layers through attention output / O / MLP
     pairs = (L - 1) * n * n / 2.0 + n if last_row_only else L * n * n / 2.0
+    # MLP: layers whose MLP rows exceed 256 run the fused gate/up + down launch (mlp_fused, when enabled); the last
+    # layer's single row (last_row_only) runs the separate GEMMs
+    fused_rows = ((L - 1) * n if last_row_only else L * n) if n > 256 else 0
+    sep_rows = rows - fused_rows
     return {"gemm_qkv_rope": 2.0 * n * h * qkvc * L, "gemm_o_resid": 2.0 * rows * ctx * h,
-            "gemm_gate_up_silu": 2.0 * rows * h * 2 * I, "gemm_down_resid": 2.0 * rows * I * h,
+            "gemm_gate_up_silu": 2.0 * sep_rows * h * 2 * I, "gemm_down_resid": 2.0 * sep_rows * I * h,
+            "mlp_fused": 2.0 * fused_rows * h * 3 * I,
+            "gemm_gate_up_silu_if_separate": 2.0 * rows * h * 2 * I, "gemm_down_resid_if_separate": 2.0 * rows * I * h,
             "attention": 4.0 * h * pairs}
 
 
@@ -505,6 +511,9 @@ def main():
     if tpath.exists():
         traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch", {})
     by_kernel = {}
+    if prof.get("mlp_fused", (0, 0))[1] == 0:  # per-chunk MLP launches (PO_FUSED_MLP=0): all MLP rows separate
+        cls_flops["gemm_gate_up_silu"] = cls_flops["gemm_gate_up_silu_if_separate"]
+        cls_flops["gemm_down_resid"] = cls_flops["gemm_down_resid_if_separate"]
     for name, (ms, cnt) in prof.items():
         if cnt == 0:
             continue  # kernel classes this forward does not launch (norm folded into GEMMs, gather in A/B mode only)

@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "attention.cuh"
 #include "stream.cuh"
+#include "mlp.cuh"
 #include <cmath>
 #include <cstring>
 #include <cstdio>
@@ -116,7 +117,11 @@ struct po_engine {
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
   // persistent weight-streaming kernel (prefix hits): partial tiles, fix-up flags, grid-barrier counter
-  unsigned int* lm_ticket = nullptr;  // multi-CTA LM head: CTAs finished (the last one runs the softmax)
+  unsigned int* lm_ticket = nullptr;
+  int* mlp_cnt = nullptr;                 // fused MLP launch: per-piece completion counters + exit ticket
+  unsigned int* mlp_ticket = nullptr;
+  int* mlp_next = nullptr;
+  int mlp_piece_max = 0;                  // rows per piece of the act ring (two pieces = chunk rows)  // multi-CTA LM head: CTAs finished (the last one runs the softmax)
   float* sk_ws = nullptr;       // stream-K short-launch GEMMs: per-CTA partial slots and flags (gemm_sk.cu)
   uint32_t* sk_flags = nullptr;
   uint32_t sk_epoch = 0;
@@ -400,6 +405,16 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
     if (gw && dalloc(e, &e->gemm_ws, gw, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "GEMM workspace failed");
     if (dalloc(e, &e->lm_ticket, 4, &e->workspace_bytes)) return fail(PO_ERR_CUDA, "LM head counter failed");
     cudaMemsetAsync(e->lm_ticket, 0, 4, s);
+    if (!f8 && chunk_rows >= 512) {  // fused MLP: the act buffer is a two-piece ring
+      e->mlp_piece_max = (int)(chunk_rows / 2);
+      const size_t nc = po::mlp_counter_ints(T, e->mlp_piece_max);
+      if (dalloc(e, &e->mlp_cnt, nc * 4, &e->workspace_bytes) || dalloc(e, &e->mlp_ticket, 4, &e->workspace_bytes) ||
+          dalloc(e, &e->mlp_next, 4, &e->workspace_bytes))
+        return fail(PO_ERR_CUDA, "MLP counters failed");
+      cudaMemsetAsync(e->mlp_cnt, 0, nc * 4, s);
+      cudaMemsetAsync(e->mlp_ticket, 0, 4, s);
+      cudaMemsetAsync(e->mlp_next, 0, 4, s);
+    }
     if (!f8) {  // stream-K short-launch GEMMs
       if (dalloc(e, &e->sk_ws, po::gemm_sk_ws_bytes(), &e->workspace_bytes) ||
           dalloc(e, &e->sk_flags, po::gemm_sk_flag_bytes(), &e->workspace_bytes))
@@ -745,7 +760,7 @@ bool pool_direct_enabled() {
 }
 
 enum KClass { KC_EMBED = 0, KC_NORM, KC_GATHER, KC_QKV, KC_SCATTER, KC_ATTN, KC_O, KC_GATE_UP, KC_DOWN, KC_LM_HEAD,
-              KC_STREAM, KC_COUNT };
+              KC_STREAM, KC_MLP, KC_COUNT };
 
 // PO_STREAM=1 runs prefix hits' layer GEMMs through the persistent streaming kernel (stream.cu). Off by default:
 // its mainloop streams weights faster than the per-GEMM launches, but the in-kernel split-tile fix-up is
@@ -897,9 +912,34 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
     norm_out(go, e->xg + (size_t)row0 * h, ly.mlp_norm, e->ss_mlp + (size_t)row0 * nseg);
     rc |= run_gemm(KC_O, e->map_ctx, e->xn, ctxc, ly.map_o, ly.map2_o, ly.map3_o, po::EPI_RESID_F32, go,
                    e->map_ctx8, e->ctx8, e->ctx_s, ly.f8_o, ly.s_o);
+    const int mlp_rows = n_miss - row0;
+    if (!rc && e->mlp_cnt && mlp_rows > 256 && po::mlp_fused_enabled()) {
+      // the whole MLP of the layer in one launch: gate/up and down tiles of balanced row pieces, the intermediate in
+      // the L2-pinned two-piece ring (mlp.cu)
+      po::MlpArgs ma{};
+      ma.rows = mlp_rows;
+      const int npc = (mlp_rows + e->mlp_piece_max - 1) / e->mlp_piece_max;
+      ma.piece = (mlp_rows + npc - 1) / npc;
+      ma.cnt = e->mlp_cnt;
+      ma.ticket = e->mlp_ticket;
+      ma.next = e->mlp_next;
+      po::GemmArgs& gu = ma.gu;
+      gu.M = mlp_rows; gu.N = 2 * I; gu.K = h; gu.a_row0 = row0;
+      gu.out = e->act; gu.ldo = I;
+      norm_in(gu, e->ss_mlp + (size_t)row0 * nseg);
+      po::GemmArgs& gd = ma.dn;
+      gd.M = mlp_rows; gd.N = h; gd.K = I;
+      gd.resid = e->resid + (size_t)row0 * h; gd.ldr = h;
+      norm_out(gd, e->xg + (size_t)row0 * h, gamma_next_layer, e->ss_attn + (size_t)row0 * nseg);
+      mark(KC_MLP, true);
+      rc |= po::mlp_launch(e->map_xg, ly.map2_gu, e->map_act, ly.map2_down, ma, s);
+      mark(KC_MLP, false);
+      ++launches;
+      if (l + 1 < L) rc |= qkv_gemm(l + 1);
+      continue;
+    }
     // balanced chunks: ceil(rows / chunk) pieces of equal size (<= chunk), so no piece is a short tail whose GEMMs
     // leave most SM pairs idle (20,000 rows at chunk 2304: nine pieces of 2,223 rows = 9 x 256-row tiles each)
-    const int mlp_rows = n_miss - row0;
     const int n_pieces = (mlp_rows + c.chunk - 1) / c.chunk;
     const int piece = n_pieces > 0 ? (mlp_rows + n_pieces - 1) / n_pieces : c.chunk;
     for (int lo = row0; lo < n_miss && !rc; lo += piece) {

