@@ -186,22 +186,42 @@ constexpr int pair_threads() { return 128 + 128 * EW; }
 template <bool F8, int BNT>
 constexpr int pair_ew() { return 1; }
 
+// RT (EPI_RESID_F32, bf16, 256-wide tiles): the residual read-modify-write goes through shared memory by TMA. Per
+// epilogue warp and 32-column chunk, a [32 rows x 32 fp32] box of the residual is loaded one chunk ahead (128-byte
+// swizzle: float4 q of row r at q ^ (r & 7), conflict-free for the thread-per-row access), updated in place, and
+// stored back with the bf16 folded-norm input box by TMA, instead of per-thread 128-byte row segments (32 L2 lines
+// per warp instruction, in both directions). One pipeline stage fewer pays for the 48 KB of staging.
+constexpr int RT_WARP_BYTES = 2 * 4096 + 2 * 2048;  // per epilogue warp: two residual boxes + two xg boxes
+template <int EPI, int BNT, bool F8>
+constexpr bool pair_rt() { return EPI == EPI_RESID_F32 && BNT == 256 && !F8; }
+template <int EPI, int BNT, bool F8>
+constexpr int pair_stages() { return pair_rt<EPI, BNT, F8>() ? Pair<BNT>::STAGES - 1 : Pair<BNT>::STAGES; }
+template <int EPI, int BNT, bool F8>
+constexpr int pair_smem() {
+  return pair_stages<EPI, BNT, F8>() * Pair<BNT>::STAGE + (pair_rt<EPI, BNT, F8>() ? 4 * RT_WARP_BYTES : 0) + 1024 +
+         256;
+}
+
 template <int EPI, int BNT, bool F8 = false, int EW = pair_ew<F8, BNT>()>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_r, const __grid_constant__ CUtensorMap map_xo,
                  const GemmArgs args) {
   constexpr int KE = F8 ? 2 * BK : BK;  // k elements per k-block
-  constexpr int STAGES2 = Pair<BNT>::STAGES;
+  constexpr bool RT = pair_rt<EPI, BNT, F8>();
+  constexpr int STAGES2 = pair_stages<EPI, BNT, F8>();
   constexpr int B_HALF = Pair<BNT>::B_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES2 * HALF_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * Pair<BNT>::STAGE);
+  uint8_t* rt_stg = smem + STAGES2 * Pair<BNT>::STAGE;  // RT staging (4 warps x RT_WARP_BYTES)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(rt_stg + (RT ? 4 * RT_WARP_BYTES : 0));
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* rt_bar = tempty_bar + 2;  // [4 warps][2 buffers] residual box loads (RT)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rt_bar + 8);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -226,6 +246,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 2);  // one arrival per CTA of the pair (leader's copy is the one used)
     }
+    if (RT)
+      for (int s = 0; s < 8; ++s) mbar_init(&rt_bar[s], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, 2 * BNT);
@@ -318,6 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
     constexpr int CW = BNT / EW;  // columns per epilogue warp of a quadrant
     const int part = (warp - 4) >> 2;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    int rt_ph[2] = {0, 0};  // RT: parity of each residual buffer's next load
     int it = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
       int mb, nb;
@@ -328,11 +351,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
       tc_fence_after();
       const int row = mb * 2 * BM + rank * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BNT;
-      epilogue_tile<EPI, BNT, F8>(args, taddr, row, nb, ksp, t, PartSrc{}, part * CW, (part + 1) * CW);
+      if constexpr (RT) {
+        if (ksp > 1) {
+          epilogue_tile<EPI, BNT, F8>(args, taddr, row, nb, ksp, t, PartSrc{}, part * CW, (part + 1) * CW);
+        } else {
+          uint8_t* wst = rt_stg + wq * RT_WARP_BYTES;
+          uint64_t* rb = rt_bar + wq * 2;
+          const int r0w = mb * 2 * BM + rank * BM + wq * 32;
+          const bool xo = args.xg_out != nullptr;
+          auto load = [&](int c) {  // residual box of chunk c into buffer c & 1
+            if (lane == 0) {
+              bulk_wait_read<0>();  // the store that last read this buffer is done with it
+              mbar_arrive_expect_tx(&rb[c & 1], 4096);
+              tma_load_2d(wst + (c & 1) * 4096, &map_r, &rb[c & 1], nb * BNT + c * 32, r0w);
+            }
+          };
+          load(0);
+          load(1);
+          float sq[2] = {0.f, 0.f};
+#pragma unroll 1
+          for (int c = 0; c < BNT / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * 32, r);
+            tmem_ld_wait();
+            mbar_wait(&rb[c & 1], (uint32_t)rt_ph[c & 1]);
+            rt_ph[c & 1] ^= 1;
+            float4* rowp = reinterpret_cast<float4*>(wst + (c & 1) * 4096 + lane * 128);
+            uint32_t* xgp = reinterpret_cast<uint32_t*>(wst + 8192 + (c & 1) * 2048 + lane * 64);
+            const float4* g4 = reinterpret_cast<const float4*>(args.g_next + nb * BNT + c * 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 v = rowp[q ^ (lane & 7)];
+              v.x += __uint_as_float(r[4 * q + 0]);
+              v.y += __uint_as_float(r[4 * q + 1]);
+              v.z += __uint_as_float(r[4 * q + 2]);
+              v.w += __uint_as_float(r[4 * q + 3]);
+              rowp[q ^ (lane & 7)] = v;
+              if (xo) {
+                const float4 g = g4[q];
+                xgp[2 * q] = pack_bf16(v.x * g.x, v.y * g.y);
+                xgp[2 * q + 1] = pack_bf16(v.z * g.z, v.w * g.w);
+                sq[c >> 2] += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&map_r, wst + (c & 1) * 4096, nb * BNT + c * 32, r0w);
+              if (xo) tma_store_2d(&map_xo, wst + 8192 + (c & 1) * 2048, nb * BNT + c * 32, r0w);
+              bulk_commit();
+            }
+            if (c + 2 < BNT / 32) load(c + 2);
+          }
+          if (xo && args.ss_out && row < args.M) {
+            args.ss_out[(long long)row * args.ss_nseg + nb * 2] = sq[0];
+            args.ss_out[(long long)row * args.ss_nseg + nb * 2 + 1] = sq[1];
+          }
+        }
+      } else {
+        epilogue_tile<EPI, BNT, F8>(args, taddr, row, nb, ksp, t, PartSrc{}, part * CW, (part + 1) * CW);
+      }
       tc_fence_before();
       named_bar_sync(1, 128 * EW);
       if (threadIdx.x == 128) mbar_arrive_cluster(tempty0 + acc * 8);
     }
+    if (RT && lane == 0) bulk_wait_all();  // residual / xg stores complete before the grid does
   }
 
   tc_fence_before();
@@ -430,6 +513,22 @@ int make_tmap_store_3d(CUtensorMap* map, const void* base, bool f32, uint64_t d0
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// 2-D map for the RT epilogue: 32 x 32 boxes over an fp32 (128-byte swizzle) or bf16 (no swizzle) [rows, cols] matrix
+int make_tmap_2d_epi(CUtensorMap* map, const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes,
+                     bool swizzle128) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -498,7 +597,7 @@ size_t gemm_split_ws_bytes(int M, int N, int K) {
 template <int EPI, int BNT, bool F8 = false>
 static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, const GemmArgs& in,
                          cudaStream_t stream) {
-  ensure_smem_attr<gemm2_kernel<EPI, BNT, F8>>(Pair<BNT>::SMEM);
+  ensure_smem_attr<gemm2_kernel<EPI, BNT, F8>>(pair_smem<EPI, BNT, F8>());
   GemmArgs args = in;
   args.k_splits = 1;
   const int tiles_mn = ((args.M + 2 * BM - 1) / (2 * BM)) * (args.N / BNT);
@@ -521,8 +620,17 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
   }
   const int tiles = tiles_mn * args.k_splits;
   const int npairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  launch_pdl(gemm2_kernel<EPI, BNT, F8>, dim3(2 * npairs), dim3(pair_threads<pair_ew<F8, BNT>()>()), Pair<BNT>::SMEM, stream, map_a, map_b2,
-             args);
+  // RT: residual / folded-norm-input maps over this launch's rows (32 x 32 boxes; rows >= M clipped by TMA)
+  CUtensorMap map_r{}, map_xo{};
+  if constexpr (pair_rt<EPI, BNT, F8>()) {
+    if (args.k_splits == 1) {
+      if (make_tmap_2d_epi(&map_r, args.resid, true, args.N, args.M, (uint64_t)args.ldr * 4, true) ||
+          (args.xg_out && make_tmap_2d_epi(&map_xo, args.xg_out, false, args.N, args.M, (uint64_t)args.ldxg * 2, false)))
+        return -2;
+    }
+  }
+  launch_pdl(gemm2_kernel<EPI, BNT, F8>, dim3(2 * npairs), dim3(pair_threads<pair_ew<F8, BNT>()>()),
+             pair_smem<EPI, BNT, F8>(), stream, map_a, map_b2, map_r, map_xo, args);
   if (args.k_splits > 1) {
     const long long total = (long long)args.M * (args.N / 4);
     const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
