@@ -193,7 +193,7 @@ constexpr int pair_ew() { return 1; }
 // per warp instruction, in both directions). One pipeline stage fewer pays for the 48 KB of staging.
 constexpr int RT_WARP_BYTES = 2 * 4096 + 2 * 2048;  // per epilogue warp: two residual boxes + two xg boxes
 template <int EPI, int BNT, bool F8>
-constexpr bool pair_rt() { return EPI == EPI_RESID_F32 && BNT == 256 && !F8; }
+constexpr bool pair_rt() { return EPI == EPI_RESID_F32 && BNT == 256; }
 template <int EPI, int BNT, bool F8>
 constexpr int pair_stages() { return pair_rt<EPI, BNT, F8>() ? Pair<BNT>::STAGES - 1 : Pair<BNT>::STAGES; }
 template <int EPI, int BNT, bool F8>
@@ -374,6 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
             uint32_t r[32];
             tmem_ld32(taddr + c * 32, r);
             tmem_ld_wait();
+            dequant32<F8>(args, (F8 && row < args.M) ? args.a_scale[row] : 0.f, nb * BNT + c * 32, r);
             mbar_wait(&rb[c & 1], (uint32_t)rt_ph[c & 1]);
             rt_ph[c & 1] ^= 1;
             float4* rowp = reinterpret_cast<float4*>(wst + (c & 1) * 4096 + lane * 128);
