@@ -711,7 +711,7 @@ bool bounded_a_enabled();
 int gemm(const CUtensorMap& a, const void* x, long long ldx, const CUtensorMap& b1, const CUtensorMap& b2,
          const CUtensorMap& b3, int epi, const po::GemmArgs& g, cudaStream_t s) {
   if (po::gemm_swap_enabled() && g.M <= 256) {  // short launches: weight as the MMA's M operand
-    if (g.sk_ws && po::gemm_sk_enabled()) {  // stream-K: one round, in-kernel fix-up
+    if (g.sk_ws && po::gemm_sk_enabled(epi)) {  // stream-K: one round, in-kernel fix-up
       const int rc = po::gemm_launch_sk(b2, x, ldx, epi, g, s);
       if (rc != 1) return rc;
     }

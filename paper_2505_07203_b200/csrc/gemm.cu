@@ -836,7 +836,7 @@ int gemm_run(const GemmPlan& plan, int epi, const GemmArgs& in, cudaStream_t str
   args.N = plan.N;
   args.K = plan.K;
   if (gemm_swap_enabled() && args.M <= 256) {
-    if (args.sk_ws && gemm_sk_enabled()) {
+    if (args.sk_ws && gemm_sk_enabled(epi)) {
       const int rc = gemm_launch_sk(plan.map_b2, plan.A, plan.lda, epi, args, stream);
       if (rc != 1) return rc;
     }

@@ -102,7 +102,8 @@ bool gemm_swap_enabled();
 // launch is not covered.
 int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int epi, const GemmArgs& args,
                    cudaStream_t stream);
-bool gemm_sk_enabled();
+bool gemm_sk_enabled();          // any epilogue may use it (workspace needed)
+bool gemm_sk_enabled(int epi);   // this epilogue uses it
 constexpr int SK_FLAG_STRIDE = 32;  // uint32 per flag line
 size_t gemm_sk_ws_bytes();          // partial slots for every CTA of a launch
 size_t gemm_sk_flag_bytes();

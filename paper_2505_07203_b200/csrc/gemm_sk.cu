@@ -32,6 +32,7 @@
 #include "gemm.cuh"
 #include "gemm_epi.cuh"
 #include "stream.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 namespace po {
@@ -199,7 +200,12 @@ __device__ __forceinline__ void sk_rows(const GemmArgs& a, int row0, int nrows, 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     gemm_sk_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                   const GemmArgs args, int np) {
+                   const __grid_constant__ CUtensorMap map_st, const GemmArgs args, int np) {
+  // HEADFIX (epilogues with a transposed TMA-store form: SiLU.mul, bf16, fp32): the pair holding a cut tile's
+  // k-block 0 finalises the whole tile - the other contributors' partials (their first segments, dumped early) are
+  // bulk-copied into the freed stage ring, added to the TMEM values per 32-row chunk, and the chunk leaves through
+  // the same staged TMA stores as the per-GEMM swap kernel. Other epilogues use the cooperative fix-up below.
+  constexpr bool HEADFIX = EPI == EPI_SILU_MUL || EPI == EPI_BF16 || EPI == EPI_F32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sW = smem;
@@ -368,12 +374,94 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       const int col0 = sg.t * 256 + (int)rank * 128;  // the CTA's first output column of this tile
       const int slot = (int)blockIdx.x * 2 + (sg.t == first_t ? 0 : 1);  // dump slot of a cut segment
       const SkCols kc = cut ? SkCols{} : sk_cols<EPI>(args, col0 + lc, lc);
+      const bool head = HEADFIX && sg.a == 0 && sg.b < nk;  // HEADFIX: this pair finalises the cut tile
+      const bool dump = cut && !head;
+      int nq = 0;
+      if (head) {
+        // contributors pair+1 .. q1 hold the rest of the tile, each as its first segment (dump slot 0)
+        const int q1 = stream_owner(W, P, sg.t * nk + nk - 1);
+        nq = q1 - pair;
+        const uint32_t bytes = (uint32_t)M * 512;
+        if (warp == 4) {
+          bool ok;
+          uint32_t ns = 32;
+          do {
+            ok = true;
+            for (int q = pair + 1 + lane; q <= q1; q += 32)
+              ok &= (int)(ld_relaxed_u32(args.sk_flags + (size_t)((2 * q + (int)rank) * 2) * SK_FLAG_STRIDE) -
+                          args.sk_epoch) >= 0;
+            ok = __all_sync(0xffffffffu, ok);
+            if (!ok) {
+              __nanosleep(ns);
+              ns = ns < 256 ? ns * 2 : 256;
+            }
+          } while (!ok);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          fence_proxy_async_global();
+          SKT(6, lane == 0);
+          if (lane == 0) mbar_arrive_expect_tx(fx_bar, bytes * nq);
+          __syncwarp();
+          for (int q = pair + 1 + lane; q <= q1; q += 32)
+            bulk_g2s(smem + (size_t)(q - pair - 1) * bytes, args.sk_ws + (size_t)((2 * q + (int)rank) * 2) * 256 * 128,
+                     bytes, fx_bar);
+        }
+        mbar_wait(fx_bar, 0);  // the head segment is the pair's last: fx_bar's only phase of the launch
+        SKT(7, et == 0);
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < M; c0 += CH, ++nch) {
         uint32_t r[32];
         tmem_ld32(taddr + c0, r);
         tmem_ld_wait();
         const int rows = min(CH, M - c0);
+        if constexpr (HEADFIX) {
+          if (!dump) {
+            // partials of the other contributors, in k order ([M][128] fp32 each in the stage ring)
+            for (int q = 0; q < nq; ++q) {
+              const float* pp = reinterpret_cast<const float*>(smem + (size_t)q * M * 512) + (size_t)c0 * 128 + et;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (i < rows) r[i] = __float_as_uint(__uint_as_float(r[i]) + pp[i * 128]);
+            }
+            // transposed TMA-store epilogue (as gemm_swap.cu): this warp's 32 rows x 32 columns staged, one store
+            uint8_t* wb = stg + (wq * 2 + (nch & 1)) * 4096;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer (two chunks ago) is done
+            __syncwarp();
+            int sc0 = col0 + wq * 32;
+            if constexpr (EPI == EPI_F32) {
+              float* tt = reinterpret_cast<float*>(wb);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) tt[j * 32 + lane] = __uint_as_float(r[j]);
+            } else if constexpr (EPI == EPI_BF16) {
+              __nv_bfloat16* tt = reinterpret_cast<__nv_bfloat16*>(wb);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) tt[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
+            } else {
+              // weight rows in 16-row groups [gate 16 | up 16]: lanes 0..15 hold gate columns, 16..31 the matching up
+              // columns; two activation rows per step, every lane busy (see gemm_swap.cu)
+              __nv_bfloat16* tt = reinterpret_cast<__nv_bfloat16*>(wb);
+              const bool hi = lane >= 16;
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const float mine = __uint_as_float(hi ? r[j] : r[j + 1]);
+                const float other = __shfl_xor_sync(0xffffffffu, mine, 16);
+                const float g = hi ? other : __uint_as_float(r[j]);
+                const float up = hi ? __uint_as_float(r[j + 1]) : other;
+                const int row = j + (hi ? 1 : 0);
+                const float sc = s_inv[min(c0 + row, 255)];
+                tt[row * 16 + (lane & 15)] = __float2bfloat16_rn(silu_f(sc * g) * (sc * up));
+              }
+              sc0 /= 2;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&map_st, wb, sc0, c0, 0);
+              bulk_commit();
+            }
+            continue;
+          }
+        }
         if (cut) {  // the fp32 partial, straight from registers: one 128-byte line per warp and row
           float* dst = args.sk_ws + ((size_t)slot * 256 + c0) * 128 + et;
 #pragma unroll
@@ -395,12 +483,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                        return *reinterpret_cast<const float4*>(brow + i * 128 + off);
                      });
       }
-      if (cut) __threadfence();  // this thread's partial stores, before the flag below
+      if (dump) __threadfence();  // this thread's partial stores, before the flag below
       tc_fence_before();
       named_bar_sync(1, 128);
       if (et == 0) {
         mbar_arrive_cluster(tempty0 + acc * 8);
-        if (cut) {  // publish the partial
+        if (dump) {  // publish the partial
           st_release_u32(args.sk_flags + (size_t)slot * SK_FLAG_STRIDE, args.sk_epoch);
           SKT(5, true);
         }
@@ -412,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     const SkSeg last = sk_seg(max(lo, (hi - 1) / nk * nk), hi, nk);
     uint32_t fx_phase = 0;
 #pragma unroll 1
-    for (int w = 0; w < 2; ++w) {
+    for (int w = 0; w < (HEADFIX ? 0 : 2); ++w) {
       const SkSeg sg = w == 0 ? first : last;
       if (w == 1 && last.t == first.t) break;
       if (sg.a == 0 && sg.b == nk) continue;  // a whole tile: done above
@@ -493,6 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       named_bar_sync(1, 128);  // the copies of the next cut tile overwrite these rows
     }
     SKT(8, et == 0);
+    if (HEADFIX && et == 0) bulk_wait_all();  // TMA stores of the outputs complete before the CTA exits
 
   }
 
@@ -506,18 +595,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   SKT(9, threadIdx.x == 0);
 }
 
-// PO_SK=1 runs short launches through this kernel. Off by default: its mainloop streams the weights faster than the
-// per-GEMM swap kernel (gate/up 41 vs ~55 us, every SM busy in one round), but the fix-up tail (dump, flag wait,
-// per-row epilogue at ~700 cycles per row and warp) costs more than the split-K reduce launches it replaces: prefix
-// hit 7.4 vs 6.6 ms.
-bool gemm_sk_enabled() {
-  static int on = -1;
-  if (on < 0) {
+// Which short launches run through this kernel: PO_SK=0 none, PO_SK=1 every epilogue, default (unset) the HEADFIX
+// epilogues (SiLU.mul / bf16 / fp32: the prefix hit's gate/up), whose fix-up is one bulk copy plus the staged TMA
+// stores. The cooperative fix-up of the residual / RoPE epilogues measured slower than the split-K reduce launches
+// (DESIGN.md "Short-M GEMMs").
+bool gemm_sk_enabled(int epi) {
+  static int mode = -1;
+  if (mode < 0) {
     const char* v = getenv("PO_SK");
-    on = (v && v[0] == '1') ? 1 : 0;
+    mode = !v ? 2 : (v[0] == '1' ? 1 : 0);
   }
-  return on == 1;
+  if (mode == 1) return true;
+  return mode == 2 && (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32);
 }
+bool gemm_sk_enabled() { return gemm_sk_enabled(-1) || getenv("PO_SK") == nullptr; }
 
 size_t gemm_sk_ws_bytes() { return (size_t)num_sms() * 2 * 256 * 128 * sizeof(float); }
 size_t gemm_sk_flag_bytes() { return (size_t)num_sms() * 2 * SK_FLAG_STRIDE * sizeof(uint32_t); }
@@ -530,13 +621,33 @@ int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int e
   const int np = (args.M + 15) / 16 * 16;
   const long long W = (long long)(args.N / 256) * (args.K / BK);
   const int P = (int)(W < num_sms() / 2 ? W : num_sms() / 2);
-  CUtensorMap map_x;
+  CUtensorMap map_x, map_st;
   if (make_tmap_2d_bf16(&map_x, x, args.K, (uint64_t)args.a_row0 + args.M, ldx * 2, BK, np / 2)) return -2;
+  map_st = map_x;  // unused unless HEADFIX
+  if (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32) {
+    // HEADFIX: the head pair holds every other contributor's [M][128] fp32 partial in its stage ring
+    const int nk = args.K / BK;
+    int maxc = 1;
+    for (int t = 0; t < args.N / 256; ++t)
+      maxc = std::max(maxc, stream_owner(W, P, t * nk + nk - 1) - stream_owner(W, P, t * nk) + 1);
+    if ((size_t)(maxc - 1) * args.M * 512 > (size_t)STAGES * STAGE) return 1;
+    int mrc;
+    if (epi == EPI_F32)
+      mrc = make_tmap_store_3d(&map_st, args.out, true, args.N, args.M, 1, (uint64_t)args.ldo * 4,
+                               (uint64_t)args.ldo * 4 * args.M, 32, 32);
+    else if (epi == EPI_BF16)
+      mrc = make_tmap_store_3d(&map_st, args.out, false, args.N, args.M, 1, (uint64_t)args.ldo * 2,
+                               (uint64_t)args.ldo * 2 * args.M, 32, 32);
+    else
+      mrc = make_tmap_store_3d(&map_st, args.out, false, args.N / 2, args.M, 1, (uint64_t)args.ldo * 2,
+                               (uint64_t)args.ldo * 2 * args.M, 16, 32);
+    if (mrc) return 1;
+  }
   switch (epi) {
 #define PO_SK_CASE(E)                                                                                  \
   case E:                                                                                              \
     ensure_smem_attr<gemm_sk_kernel<E>>(SMEM);                                                         \
-    launch_pdl(gemm_sk_kernel<E>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, args, np);        \
+    launch_pdl(gemm_sk_kernel<E>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, map_st, args, np); \
     break;
     PO_SK_CASE(EPI_BF16)
     PO_SK_CASE(EPI_F32)

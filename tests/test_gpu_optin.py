@@ -25,6 +25,7 @@ def _run(args, **switches):
 
 def test_stream_k_short_gemms():
     _run(["tests/test_gpu_gemm.py", "-k", "swap or splitk"], PO_SK="1")
+    _run(["tests/test_gpu_gemm.py", "-k", "swap or splitk"], PO_SK="0")
 
 
 def test_stream_k_engine_against_oracle():
