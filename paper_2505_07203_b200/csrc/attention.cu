@@ -200,6 +200,130 @@ __device__ __forceinline__ void softmax_tile1(uint32_t s_addr, uint32_t o_addr, 
 }
 
 
+// ATTN_SPLIT_S=1 (build-time A/B): S in two N = 64 halves, the first half's softmax overlapping the second half's
+// MMA. Bit-identical results, but measured slower (20k: 1279 vs 1394 TFLOP/s, 64k: 1180 vs 1278; two waits and TMEM
+// load rounds per tile, 24 bytes of spills): off.
+#ifndef ATTN_SPLIT_S
+#define ATTN_SPLIT_S 0
+#endif
+// One P chunk c (keys 32c .. 32c+31) of this row: x = s*sl2 - m, exp2 (MUFU or the FMA-pipe polynomial), the row sum
+// in acc0/acc1 (pairs alternate), bf16 P stored over S columns [16c, 16c+16). Same arithmetic as softmax_tile1.
+template <bool MASKED>
+__device__ __forceinline__ void p_chunk(const uint32_t (&v)[128], int c, uint32_t s_addr, int lim, uint64_t sc2,
+                                        uint64_t nm2, uint64_t& acc0, uint64_t& acc1) {
+  uint32_t p[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int col = 32 * c + 2 * e;
+    float x0, x1;
+    up2(ffma2(pk2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2), x0, x1);
+    if (!MASKED && (e % POLY_DEN) >= POLY_DEN - POLY_NUM) {
+      exp2_poly2(x0, x1, x0, x1);
+    } else {
+      x0 = ex2_approx(x0);
+      x1 = ex2_approx(x1);
+    }
+    if (MASKED) {
+      if (col >= lim) x0 = 0.f;
+      if (col + 1 >= lim) x1 = 0.f;
+    }
+    if (e & 1)
+      acc1 = fadd2(acc1, pk2(x0, x1));
+    else
+      acc0 = fadd2(acc0, pk2(x0, x1));
+    p[e] = pack_bf16(x0, x1);
+  }
+  tmem_st16(s_addr + c * 16, p);
+}
+
+// softmax_tile1 with S arriving in two 64-key halves (ATTN_SPLIT_S): the first half is read as soon as its N = 64
+// MMA commits (s_half) and its P chunks are computed with the running max while the tensor core computes the second
+// half; the row max over all 128 keys then decides as before (rescale only when it grew by > RESCALE_THRESHOLD). If
+// it did, O is rescaled and the first half's P recomputed with the new max, so the result is bit-identical to
+// softmax_tile1. P of the first half is signalled (p_half) once the max is known to be final.
+template <bool MASKED, typename HalfFn>
+__device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, int lim, float sl2, int j, float& m,
+                                              float& l, HalfFn on_half, uint64_t* s_half_bar, uint64_t* s_full_bar) {
+  uint32_t v[128];
+  mbar_wait(s_half_bar, j & 1);
+  tc_fence_after();
+  tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(v));
+  tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+  tmem_ld_wait();
+  if (MASKED) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      if (c >= lim) v[c] = __float_as_uint(-INFINITY);
+  }
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int e = 0; e < 64; e += 8) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(v[e + 2 * k]), __uint_as_float(v[e + 2 * k + 1])));
+  }
+  // speculative first half with the running max (kept unless the whole row's max forces a rescale)
+  const bool spec = m != -INFINITY;
+  uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
+  {
+    const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(-m, -m);
+    if (spec) {
+      p_chunk<MASKED>(v, 0, s_addr, lim, sc2, nm2, acc0, acc1);
+      p_chunk<MASKED>(v, 1, s_addr, lim, sc2, nm2, acc0, acc1);
+    }
+  }
+  mbar_wait(s_full_bar, j & 1);
+  tc_fence_after();
+  tmem_ld32(s_addr + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
+  tmem_ld32(s_addr + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
+  tmem_ld_wait();
+  if (MASKED) {
+#pragma unroll
+    for (int c = 64; c < 128; ++c)
+      if (c >= lim) v[c] = __float_as_uint(-INFINITY);
+  }
+#pragma unroll
+  for (int e = 64; e < 128; e += 8) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(v[e + 2 * k]), __uint_as_float(v[e + 2 * k + 1])));
+  }
+  const float m_new = fmaxf(m, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2);
+  const bool resc = m_new > m + RESCALE_THRESHOLD;
+  const float alpha = resc ? ex2_approx(m - m_new) : 1.0f;
+  const bool redo = __any_sync(0xffffffffu, resc) || !spec;  // warp-uniform
+  if (j > 0 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tmem_ld32(o_addr + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+      tmem_st32(o_addr + c * 32, o);
+    }
+    tmem_st_wait();
+  }
+  if (resc) {
+    l *= alpha;
+    m = m_new;
+  }
+  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(-m, -m);
+  if (redo) {  // the first half again with the final max (same order of the sums as softmax_tile1)
+    acc0 = pk2(0.f, 0.f);
+    acc1 = pk2(0.f, 0.f);
+    p_chunk<MASKED>(v, 0, s_addr, lim, sc2, nm2, acc0, acc1);
+    p_chunk<MASKED>(v, 1, s_addr, lim, sc2, nm2, acc0, acc1);
+  }
+  on_half();
+  p_chunk<MASKED>(v, 2, s_addr, lim, sc2, nm2, acc0, acc1);
+  p_chunk<MASKED>(v, 3, s_addr, lim, sc2, nm2, acc0, acc1);
+  float s0, s1, s2, s3;
+  up2(acc0, s0, s1);
+  up2(acc1, s2, s3);
+  l += (s0 + s1) + (s2 + s3);
+}
+
 // -DATTN_TRACE: clock64 stamps of the pipeline events of one CTA (blockIdx.x == ATTN_TRACE) for tools/attn_trace.py
 #ifdef ATTN_TRACE
 constexpr int TRACE_EVENTS = 24, TRACE_TILES = 512;
@@ -229,7 +353,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* o_final = bars + 11;  // [2]
   uint64_t* p_half = bars + 13;   // [2] first 64 keys of P stored
   uint64_t* v_empty = bars + 15;  // [2] V stage free: both slots' P.V MMAs of the tile are done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* s_half = bars + 17;   // [2] first 64 keys of S computed (ATTN_SPLIT_S)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -283,7 +408,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&map);
-    for (int i = 0; i < 17; ++i) mbar_init(&bars[i], (i == 9 || i == 10 || i == 13 || i == 14) ? 128 : 1);
+    for (int i = 0; i < 19; ++i) mbar_init(&bars[i], (i == 9 || i == 10 || i == 13 || i == 14) ? 128 : 1);
     fence_barrier_init();
   }
   if (warp == 10) tmem_alloc(tmem_slot, 512);
@@ -375,9 +500,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // issues the MMAs and commits
     {
       const bool issuer = elect_one();
-      constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATTN_SPLIT_S ? 64 : 128, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, 128, false, true);
       auto issue_s = [&](int i, int st) {
+#if ATTN_SPLIT_S
+        // two N = 64 halves (keys 0..63, then 64..127 = +64 rows of the K tile), committed separately
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * BOX_BYTES + (kk & 3) * 32;
+            if (issuer) mma_bf16_ss(tmem + i * 128 + h * 64, sdesc_kmajor_sw128(smem_u32(sQ + i * TILE_BYTES + off)),
+                        sdesc_kmajor_sw128(smem_u32(sK + st * TILE_BYTES + off + h * 64 * 128)), idesc_s, kk > 0);
+          }
+          if (issuer) mma_commit(h == 0 ? &s_half[i] : &s_full[i]);
+        }
+#else
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * BOX_BYTES + (kk & 3) * 32;
@@ -385,6 +523,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                       sdesc_kmajor_sw128(smem_u32(sK + st * TILE_BYTES + off)), idesc_s, kk > 0);
         }
         if (issuer) mma_commit(&s_full[i]);
+#endif
       };
       auto issue_pv_range = [&](int i, int st, bool acc, int k0, int k1) {
 #pragma unroll
@@ -457,9 +596,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool tr_lane = ((warp & 3) | lane) == 0;
     for (int j = 0; j < n_tiles; ++j) {
       if (tr_lane) TR(4 * i, j);
+#if !ATTN_SPLIT_S
       mbar_wait(&s_full[i], j & 1);
-      if (tr_lane) TR(4 * i + 1, j);
       tc_fence_after();
+#endif
+      if (tr_lane) TR(4 * i + 1, j);
       const int kbase = (t0 + j) * BKV;
       // the first 64 keys of P are signalled as soon as they are stored (the MMA warp starts that half of P.V)
       auto half = [&]() {
@@ -469,10 +610,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (tr_lane) TR(4 * i + 2, j);
       };
       // warp-uniform: only tiles crossing the diagonal of this query block pay for the mask
+#if ATTN_SPLIT_S
+      if (kbase + BKV - 1 > my_qlo)
+        softmax_tile2<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l, half, &s_half[i], &s_full[i]);
+      else
+        softmax_tile2<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l, half, &s_half[i], &s_full[i]);
+#else
       if (kbase + BKV - 1 > my_qlo)
         softmax_tile1<true>(s_addr, o_addr, pos - kbase + 1, a.scale_log2, j, m, l, half);
       else
         softmax_tile1<false>(s_addr, o_addr, BKV, a.scale_log2, j, m, l, half);
+#endif
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[i]);
