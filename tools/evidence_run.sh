@@ -16,4 +16,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm
   python tools/bench_gemm.py > $O/ev_ncu_gemm.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 7 -c 1 -o $O/ev_attn_full -f \
   python tools/bench_attn.py > $O/ev_ncu_attn.log 2>&1
+timeout 300 python tools/attn_vs_libs.py > $O/ev_attn_vs_libs.jsonl 2>&1
+timeout 300 python tools/bench_gemm.py > $O/ev_gemm_vs_cublas.jsonl 2>&1
+timeout 300 python tools/hit_classes.py > $O/ev_hit_classes.txt 2>&1
+timeout 600 python tools/bench_configs.py llama128k $O/ev_config_llama128k.json > $O/ev_128k.log 2>&1
 ls -la $O
