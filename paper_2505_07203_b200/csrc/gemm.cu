@@ -435,11 +435,40 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
   const int ncol4 = a.N / 4;
   const long long total = (long long)a.M * ncol4;
   const size_t slice = (size_t)a.M * a.N;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int row = static_cast<int>(i / ncol4);
-    const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
-    splitk_reduce_quad<EPI>(a, row, col, a.split_ws + (size_t)row * a.N + col, slice, a.k_splits);
+  constexpr bool NORM = EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE;
+  // folded-norm consumers: the 1/rms of the block's rows (a block's quads span few rows) is computed once per row by
+  // one warp - every segment sum loaded at once, then summed in segment order (row_inv_rms's order, so the result is
+  // the same) - instead of by every thread through four dependent load batches
+  __shared__ float s_ss[8][64];
+  __shared__ float s_sc[8];
+  const bool share = NORM && a.ss_in && a.ss_nseg <= 64;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < total; base += (long long)gridDim.x * blockDim.x) {
+    const long long i = base + threadIdx.x;
+    const int r_first = static_cast<int>(base / ncol4);
+    const long long last = base + blockDim.x - 1 < total ? base + blockDim.x - 1 : total - 1;
+    const int nrows = static_cast<int>(last / ncol4) - r_first + 1;
+    const bool use = share && nrows <= 8;  // uniform across the block
+    if (use) {
+      const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      if (w < nrows) {
+        const float* src = a.ss_in + (long long)(r_first + w) * a.ss_nseg;
+        for (int k = ln; k < a.ss_nseg; k += 32) s_ss[w][k] = __ldcg(src + k);
+        __syncwarp();
+        if (ln == 0) {
+          float sum = 0.f;
+          for (int k = 0; k < a.ss_nseg; ++k) sum += s_ss[w][k];
+          s_sc[w] = rsqrtf(sum / a.norm_dim + a.norm_eps);
+        }
+      }
+      __syncthreads();
+    }
+    if (i < total) {
+      const int row = static_cast<int>(i / ncol4);
+      const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
+      splitk_reduce_quad<EPI>(a, row, col, a.split_ws + (size_t)row * a.N + col, slice, a.k_splits,
+                              use ? s_sc[row - r_first] : -1.f);
+    }
+    if (use) __syncthreads();  // s_sc is rewritten by the next iteration
   }
 }
 

@@ -293,12 +293,12 @@ __device__ __forceinline__ void dq4(const GemmArgs& a, int row, int col, float4&
 // splitk_reduce_kernel (gemm.cu) and the streaming kernel's cooperative fix-up (stream.cu).
 template <int EPI>
 __device__ __forceinline__ void splitk_reduce_quad(const GemmArgs& a, int row, int col, const float* p, size_t slice,
-                                                   int splits) {
+                                                   int splits, float sc_pre = -1.f) {
   float4 acc = split_sum(p, slice, splits);
   dq4(a, row, col, acc);
   float sc = 1.0f;
   if constexpr (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
-    if (a.ss_in) sc = row_inv_rms(a, row);
+    if (a.ss_in) sc = sc_pre >= 0.f ? sc_pre : row_inv_rms(a, row);
     acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
   }
   if constexpr (EPI == EPI_BF16) {
