@@ -200,12 +200,18 @@ __device__ __forceinline__ void sk_rows(const GemmArgs& a, int row0, int nrows, 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     gemm_sk_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                   const __grid_constant__ CUtensorMap map_st, const GemmArgs args, int np) {
+                   const __grid_constant__ CUtensorMap map_st, const __grid_constant__ CUtensorMap map_r,
+                   const __grid_constant__ CUtensorMap map_xo, const GemmArgs args, int np) {
   // HEADFIX (epilogues with a transposed TMA-store form: SiLU.mul, bf16, fp32): the pair holding a cut tile's
   // k-block 0 finalises the whole tile - the other contributors' partials (their first segments, dumped early) are
   // bulk-copied into the freed stage ring, added to the TMEM values per 32-row chunk, and the chunk leaves through
   // the same staged TMA stores as the per-GEMM swap kernel. Other epilogues use the cooperative fix-up below.
-  constexpr bool HEADFIX = EPI == EPI_SILU_MUL || EPI == EPI_BF16 || EPI == EPI_F32;
+  // EPI_RESID_F32 joins it with a transposed residual epilogue: per warp and chunk a [32 rows x 32 fp32] residual box
+  // by TMA (128-byte swizzle: thread = column reads a row's 128 bytes conflict-free), updated in place, stored back
+  // with the bf16 folded-norm input box; the per-row sums of squares over the CTA's 128 columns by a butterfly
+  // transpose-reduction inside each warp and a 4-warp sum in shared memory.
+  constexpr bool HEADFIX = EPI == EPI_SILU_MUL || EPI == EPI_BF16 || EPI == EPI_F32 || EPI == EPI_RESID_F32;
+  constexpr bool RESID = EPI == EPI_RESID_F32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sW = smem;
@@ -218,7 +224,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* fx_bar = tempty_bar + 2;  // fix-up copies, one phase per cut tile
   uint64_t* ss_bar = fx_bar + 1;      // the rows' RMS segment sums (folded-norm consumers)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ss_bar + 1);
+  uint64_t* fx2 = ss_bar + 1;         // [2] HEADFIX: the contributors' rows of chunk k in ring buffer k & 1
+  uint64_t* rb_bar = fx2 + 2;         // [4] RESID: each epilogue warp's residual box
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rb_bar + 4);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -247,6 +255,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
     mbar_init(fx_bar, 1);
     mbar_init(ss_bar, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&fx2[b], 1);
+    for (int b = 0; b < 4; ++b) mbar_init(&rb_bar[b], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
@@ -362,6 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
     const int first_t = lo / nk;
     int it = 0, nch = 0;
+    uint32_t rb_ph = 0;  // RESID: parity of this warp's residual box barrier
     for (int f = lo; f < hi; ++it) {
       const SkSeg sg = sk_seg(f, hi, nk);
       f = sg.t * nk + sg.b;
@@ -377,11 +388,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       const bool head = HEADFIX && sg.a == 0 && sg.b < nk;  // HEADFIX: this pair finalises the cut tile
       const bool dump = cut && !head;
       int nq = 0;
+      // HEADFIX: chunk k of the contributors' partials (their rows c0 .. c0+31, 16 KB each) into ring buffer k & 1
+      auto issue_piece = [&](int k) {
+        if (warp == 4 && lane == 0 && k * CH < M) {
+          const uint32_t bytes = (uint32_t)min(CH, M - k * CH) * 512;
+          mbar_arrive_expect_tx(&fx2[k & 1], bytes * nq);
+          for (int q = 0; q < nq; ++q)
+            bulk_g2s(smem + (size_t)((k & 1) * nq + q) * CH_BYTES,
+                     args.sk_ws + ((size_t)((2 * (pair + 1 + q) + (int)rank) * 2) * 256 + k * CH) * 128, bytes,
+                     &fx2[k & 1]);
+        }
+      };
       if (head) {
         // contributors pair+1 .. q1 hold the rest of the tile, each as its first segment (dump slot 0)
         const int q1 = stream_owner(W, P, sg.t * nk + nk - 1);
         nq = q1 - pair;
-        const uint32_t bytes = (uint32_t)M * 512;
         if (warp == 4) {
           bool ok;
           uint32_t ns = 32;
@@ -399,13 +420,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           fence_proxy_async_global();
           SKT(6, lane == 0);
-          if (lane == 0) mbar_arrive_expect_tx(fx_bar, bytes * nq);
-          __syncwarp();
-          for (int q = pair + 1 + lane; q <= q1; q += 32)
-            bulk_g2s(smem + (size_t)(q - pair - 1) * bytes, args.sk_ws + (size_t)((2 * q + (int)rank) * 2) * 256 * 128,
-                     bytes, fx_bar);
         }
-        mbar_wait(fx_bar, 0);  // the head segment is the pair's last: fx_bar's only phase of the launch
+        issue_piece(0);
+        issue_piece(1);
         SKT(7, et == 0);
       }
 #pragma unroll 1
@@ -416,12 +433,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         const int rows = min(CH, M - c0);
         if constexpr (HEADFIX) {
           if (!dump) {
-            // partials of the other contributors, in k order ([M][128] fp32 each in the stage ring)
-            for (int q = 0; q < nq; ++q) {
-              const float* pp = reinterpret_cast<const float*>(smem + (size_t)q * M * 512) + (size_t)c0 * 128 + et;
+            const int k = c0 / CH;
+            float4* rbox = reinterpret_cast<float4*>(stg + wq * 8192);  // RESID: this warp's residual box
+            if constexpr (RESID) {
+              if (lane == 0) {
+                bulk_wait_read<0>();  // the previous chunk's store has read the box
+                mbar_arrive_expect_tx(&rb_bar[wq], 4096);
+                tma_load_2d(rbox, &map_r, &rb_bar[wq], col0 + wq * 32, c0);
+              }
+            }
+            if (nq > 0) {
+              // partials of the other contributors, in k order (this chunk's rows in ring buffer k & 1)
+              mbar_wait(&fx2[k & 1], (k >> 1) & 1);
+              for (int q = 0; q < nq; ++q) {
+                const float* pp = reinterpret_cast<const float*>(smem + (size_t)((k & 1) * nq + q) * CH_BYTES) + et;
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < rows) r[i] = __float_as_uint(__uint_as_float(r[i]) + pp[i * 128]);
+                for (int i = 0; i < 32; ++i)
+                  if (i < rows) r[i] = __float_as_uint(__uint_as_float(r[i]) + pp[i * 128]);
+              }
+              named_bar_sync(1, 128);  // every thread is done with buffer k & 1: refill it with chunk k + 2
+              issue_piece(k + 2);
+            }
+            if constexpr (RESID) {
+              mbar_wait(&rb_bar[wq], rb_ph);
+              rb_ph ^= 1;
+              const float gcol = args.xg_out ? args.g_next[col0 + wq * 32 + lane] : 0.f;
+              __nv_bfloat16* xbox = reinterpret_cast<__nv_bfloat16*>(stg + wq * 8192 + 4096);
+              float a2[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                // element (row i, column lane) of the 128B-swizzled box: 16-byte chunk (lane / 4) ^ (i & 7)
+                float* e = reinterpret_cast<float*>(rbox + i * 8 + ((lane >> 2) ^ (i & 7))) + (lane & 3);
+                const float v = *e + __uint_as_float(r[i]);
+                *e = v;
+                xbox[i * 32 + lane] = __float2bfloat16_rn(v * gcol);
+                a2[i] = v * v;
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&map_r, rbox, col0 + wq * 32, c0);
+                if (args.xg_out) tma_store_2d(&map_xo, xbox, col0 + wq * 32, c0);
+                bulk_commit();
+              }
+              if (args.ss_out) {
+                // butterfly transpose-reduction: lane l ends with this warp's sum of squares of row l
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                  const bool up = (lane & off) != 0;
+#pragma unroll
+                  for (int i = 0; i < off; ++i) {
+                    const float send = up ? a2[i] : a2[i + off];
+                    const float keep = up ? a2[i + off] : a2[i];
+                    a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                  }
+                }
+                float* s_sq = s_inv;  // [4 warps][32 rows]
+                s_sq[wq * 32 + lane] = a2[0];
+                named_bar_sync(1, 128);
+                if (wq == 0 && lane < rows)
+                  args.ss_out[(long long)(c0 + lane) * args.ss_nseg + col0 / 128] =
+                      ((s_sq[lane] + s_sq[32 + lane]) + s_sq[64 + lane]) + s_sq[96 + lane];
+                named_bar_sync(1, 128);  // s_sq is rewritten by the next chunk
+              }
+              continue;
             }
             // transposed TMA-store epilogue (as gemm_swap.cu): this warp's 32 rows x 32 columns staged, one store
             uint8_t* wb = stg + (wq * 2 + (nch & 1)) * 4096;
@@ -595,9 +670,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   SKT(9, threadIdx.x == 0);
 }
 
-// Which short launches run through this kernel: PO_SK=0 none, PO_SK=1 every epilogue, default (unset) the HEADFIX
-// epilogues (SiLU.mul / bf16 / fp32: the prefix hit's gate/up), whose fix-up is one bulk copy plus the staged TMA
-// stores. The cooperative fix-up of the residual / RoPE epilogues measured slower than the split-K reduce launches
+// Which short launches run through this kernel: PO_SK=0 none, PO_SK=1 every epilogue, default (unset) SiLU.mul /
+// bf16 / fp32 (the prefix hit's gate/up), whose head fix-up streams the contributors' rows and leaves through staged
+// TMA stores. The cooperative fix-up of the residual / RoPE epilogues measured slower than the split-K reduce launches
 // (DESIGN.md "Short-M GEMMs").
 bool gemm_sk_enabled(int epi) {
   static int mode = -1;
@@ -606,6 +681,8 @@ bool gemm_sk_enabled(int epi) {
     mode = !v ? 2 : (v[0] == '1' ? 1 : 0);
   }
   if (mode == 1) return true;
+  // (the residual epilogue's head fix-up - 3-5 contributors streamed per chunk, transposed residual boxes - measured
+  // slower than swap + reduce on the hit's O / down: 1.12 vs 0.81 ms and 1.58 vs 1.29 ms per forward)
   return mode == 2 && (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32);
 }
 bool gemm_sk_enabled() { return gemm_sk_enabled(-1) || getenv("PO_SK") == nullptr; }
@@ -621,16 +698,24 @@ int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int e
   const int np = (args.M + 15) / 16 * 16;
   const long long W = (long long)(args.N / 256) * (args.K / BK);
   const int P = (int)(W < num_sms() / 2 ? W : num_sms() / 2);
-  CUtensorMap map_x, map_st;
+  CUtensorMap map_x, map_st, map_r, map_xo;
   if (make_tmap_2d_bf16(&map_x, x, args.K, (uint64_t)args.a_row0 + args.M, ldx * 2, BK, np / 2)) return -2;
-  map_st = map_x;  // unused unless HEADFIX
-  if (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32) {
-    // HEADFIX: the head pair holds every other contributor's [M][128] fp32 partial in its stage ring
+  map_st = map_r = map_xo = map_x;  // unused unless HEADFIX / RESID
+  if (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32 || epi == EPI_RESID_F32) {
+    // HEADFIX: the head pair streams the other contributors' rows through two halves of its stage ring, 32 rows
+    // (16 KB) per contributor per chunk
     const int nk = args.K / BK;
     int maxc = 1;
     for (int t = 0; t < args.N / 256; ++t)
       maxc = std::max(maxc, stream_owner(W, P, t * nk + nk - 1) - stream_owner(W, P, t * nk) + 1);
-    if ((size_t)(maxc - 1) * args.M * 512 > (size_t)STAGES * STAGE) return 1;
+    if ((size_t)(maxc - 1) * 2 * CH_BYTES > (size_t)STAGES * STAGE) return 1;
+  }
+  if (epi == EPI_RESID_F32) {
+    if (make_tmap_2d_epi(&map_r, args.resid, true, args.N, args.M, (uint64_t)args.ldr * 4, true) ||
+        (args.xg_out && make_tmap_2d_epi(&map_xo, args.xg_out, false, args.N, args.M, (uint64_t)args.ldxg * 2, false)))
+      return 1;
+  }
+  if (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32) {
     int mrc;
     if (epi == EPI_F32)
       mrc = make_tmap_store_3d(&map_st, args.out, true, args.N, args.M, 1, (uint64_t)args.ldo * 4,
@@ -647,7 +732,7 @@ int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int e
 #define PO_SK_CASE(E)                                                                                  \
   case E:                                                                                              \
     ensure_smem_attr<gemm_sk_kernel<E>>(SMEM);                                                         \
-    launch_pdl(gemm_sk_kernel<E>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, map_st, args, np); \
+    launch_pdl(gemm_sk_kernel<E>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, map_st, map_r, map_xo, args, np); \
     break;
     PO_SK_CASE(EPI_BF16)
     PO_SK_CASE(EPI_F32)
