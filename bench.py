@@ -121,7 +121,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------------- CPU arm
-REF_SIZES = (1024, 2048, 4096)
+REF_SIZES = (4096, 8192, 20_000)  # the last is the BASELINE request length: measured, not extrapolated
 
 
 def _stock_numerics():
@@ -167,6 +167,11 @@ class StockReference:
         return float(a), float(b)
 
     def request_seconds(self, n_tokens: int) -> float:
+        """32 layers x the measured layer time at n_tokens when that length was timed (the fit over small sizes
+        underestimated a 20k layer by 1.39x: profiles/r2_reference_fit_check.json), else the fit."""
+        at_n = [t for n, t in self.samples if n == n_tokens]
+        if at_n:
+            return self.M.num_layers * statistics.median(at_n)
         a, b = self.fit()
         return self.M.num_layers * (a * n_tokens + b * n_tokens * n_tokens)
 
@@ -177,7 +182,9 @@ class StockReference:
             per.setdefault(n, []).append(t)
         return {"layer_seconds": {str(n): statistics.median(v) for n, v in sorted(per.items())},
                 "fit_s": {"a_per_token": a, "b_per_token2": b},
-                "request_seconds_extrapolated": self.request_seconds(n_tokens)}
+                "request_seconds": self.request_seconds(n_tokens),
+                "request_from": "32 x measured layer" if any(n == n_tokens for n, _ in self.samples)
+                                else "fit extrapolation"}
 
 
 def cpu_layer_sample(n: int = 1024, seed: int = 0):
@@ -263,8 +270,8 @@ def cpu_baseline_sample(n_tokens: int) -> dict:
         return {"value": n_tokens / sec, "unit": UNIT, "cores": blas_threads(), "kind": "reference",
                 "sample": f"stock prefillsim.numerics.block_forward_hybrid (baseline/_ref) at hidden 4096 / "
                           f"intermediate 14336, one layer at each of {list(REF_SIZES)} tokens "
-                          f"({', '.join(f'{float(v):.2f} s' for v in sm['layer_seconds'].values())}), fit "
-                          f"t = a n + b n^2, extrapolated to 32 layers x {n_tokens} tokens",
+                          f"({', '.join(f'{float(v):.2f} s' for v in sm['layer_seconds'].values())}); request = "
+                          f"{sm['request_from']} ({n_tokens} tokens, 32 layers)",
                 "fit": sm, "blas": blas_name(), "host_cpus": os.cpu_count()}
     run, flops = cpu_layer_sample()
     run()
@@ -305,14 +312,16 @@ def run_reference(args, world, rank):
         t_all = 0.0
         for i in range(args.steps):
             t_all += ref.step(REF_SIZES[i % len(REF_SIZES)])
-        if args.steps < 2:  # a fit needs two sizes
-            t_all += ref.step(REF_SIZES[1])
+        if not any(n == args.n_tokens for n, _ in ref.samples):  # the request length itself is always timed
+            t_all += ref.step(args.n_tokens)
+        if len({n for n, _ in ref.samples}) < 2:  # the reported fit needs two sizes
+            t_all += ref.step(REF_SIZES[0])
         request_s = ref.request_seconds(args.n_tokens)
         value = args.n_tokens / request_s
         kind = "reference"
         sample = (f"stock prefillsim.numerics.block_forward_hybrid (baseline/_ref, unmodified) at hidden 4096 / "
-                  f"intermediate 14336, one layer per step cycling {list(REF_SIZES)} tokens, fit t = a n + b n^2, "
-                  f"extrapolated to 32 layers x {args.n_tokens} tokens ({request_s:.0f} s per request)")
+                  f"intermediate 14336, one layer per step cycling {list(REF_SIZES)} tokens; request = 32 x the "
+                  f"measured {args.n_tokens}-token layer ({request_s:.0f} s per request)")
         extra = {"fit": ref.summary(args.n_tokens)}
         ms_per_step = 1e3 * t_all / max(1, len(ref.samples))
     else:
