@@ -685,21 +685,25 @@ bool gemm_pair_narrow(int M, int N) {
 // streams past them: 16 blocks of a K = 4096 operand are 32 MB, but the down projection's K = 14336 makes 16 blocks
 // 117 MB (the whole L2), and ncu showed its A re-streamed (2.8x the algorithmic reads). Long-K launches therefore
 // take PO_GROUP_LONGK blocks (default 8: 58 MB of A). The default for K <= 8192 stays 16.
-static int pair_group(int K) {
-  static int longk = -1;
+static int pair_group(int K, int N) {
+  static int longk = -1, widen = -1;
   if (longk < 0) {
     const char* v = getenv("PO_GROUP_LONGK");
     longk = v ? atoi(v) : 8;
     if (longk < 1) longk = 16;
+    const char* w = getenv("PO_GROUP_WIDEN");  // A/B: m-blocks per sweep for wide launches (N >= 16384, gate/up)
+    widen = w ? atoi(w) : 0;
   }
-  return K > 8192 ? longk : GROUP_M;
+  if (K > 8192) return longk;
+  if (widen > 0 && N >= 16384) return widen;
+  return GROUP_M;
 }
 
 template <int EPI>
 static int launch_pair(const CUtensorMap& map_a, const CUtensorMap& map_b2, const CUtensorMap* map_b3,
                        const GemmArgs& in0, cudaStream_t stream) {
   GemmArgs in = in0;
-  if (in.group_m <= 0) in.group_m = pair_group(in.K);
+  if (in.group_m <= 0) in.group_m = pair_group(in.K, in.N);
   if (map_b3 && gemm_pair_narrow(in.M, in.N)) return launch_pair_t<EPI, 128>(map_a, *map_b3, in, stream);
   return launch_pair_t<EPI, 256>(map_a, map_b2, in, stream);
 }
