@@ -52,5 +52,12 @@ with Engine(TINY_FP8, seed=1, max_tokens=1024, chunk=256, pool_blocks=64) as e:
     slots = list(range(700 // 16))
     e.prefill(t, [1, 2], 0, slots)
     e.prefill(t, [1, 2], 512, slots)
+# round 2: multi-CTA LM head (allowed list > 256 rows); an engine whose MLP runs 512-row pieces (fused MLP launch
+# under PO_FUSED_MLP=1); prefix hits through the stream-K kernel (default: gate/up; PO_SK=1: every epilogue)
+with Engine(TINY, seed=1, max_tokens=2048, chunk=1024, pool_blocks=128) as e:
+    t = np.random.default_rng(2).integers(0, 2**32, size=1300, dtype=np.uint32)
+    slots = list(range(1300 // 16))
+    e.prefill(t, list(range(0, 32000, 7)), 0, slots)
+    e.prefill(t, [1, 2], 1296 // 16 * 16 - 160, slots)
 torch.cuda.synchronize()
 print("sanitize workload done")
