@@ -680,7 +680,8 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
     lam_sweep.append({"policy": "fifo", "p99_s": rf.p99_latency, "mean_s": rf.mean_latency})
     # wall clock: serving.Server (lookahead loop, C-ABI forwards, host-side hashing / scheduling / copies inside the
     # latency) with real arrivals in real time. First its saturation throughput (every request at t = 0), then the
-    # highest of {1.0, 0.95, 0.9, 0.85, 0.8} x the virtual-clock knee whose wall-clock p99 meets the SLO.
+    # highest of {1.0, 0.95, 0.9, 0.85, 0.8} x the virtual-clock knee whose wall-clock p99 meets the SLO, refined by
+    # three bisection steps toward the next grid rate that misses it.
     wall = None
     if best:
         def wall_run(tr):
@@ -701,6 +702,20 @@ def qps_at_slo(eng, M, world, rank, slo, dist):
                          "throughput_rps": wrep.throughput, "served": wrep.served})
             if wrep.p99_latency <= slo:
                 break
+        # resolve the wall-clock knee below the grid's 5% steps: bisect between the passing rate and the failing one
+        passing = [r["rate"] for r in runs if r["p99_s"] <= slo]
+        failing = [r["rate"] for r in runs if r["p99_s"] > slo]
+        if passing and failing:
+            lo, hi = max(passing), min(f for f in failing if f > max(passing))
+            for _ in range(3):
+                q = 0.5 * (lo + hi)
+                wrep = wall_run(wl.poisson_arrivals(trace, q, seed=0, keep_sessions=True))
+                runs.append({"rate": q, "p99_s": wrep.p99_latency, "mean_s": wrep.mean_latency,
+                             "throughput_rps": wrep.throughput, "served": wrep.served})
+                if wrep.p99_latency <= slo:
+                    lo = q
+                else:
+                    hi = q
         ok = [r["rate"] for r in runs if r["p99_s"] <= slo]
         wall = {"qps_at_slo": max(ok) if ok else None, "saturation_rps": wsat.throughput,
                 "virtual_saturation_rps": sat, "runs": runs,
