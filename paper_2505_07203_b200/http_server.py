@@ -171,6 +171,9 @@ def main():
     ap.add_argument("--max-tokens", type=int, default=32768)
     ap.add_argument("--host", default="127.0.0.1")
     ap.add_argument("--port", type=int, default=8000)
+    ap.add_argument("--routing", default="round_robin", choices=["round_robin", "least_work"],
+                    help="first-seen user placement across GPUs: the reference's round robin, or least outstanding "
+                         "cache-miss work (SURVEY H9)")
     args = ap.parse_args()
     import uvicorn
 
@@ -179,7 +182,7 @@ def main():
     from .serving import Server
 
     engines = [Engine(args.model, device=d, max_tokens=args.max_tokens) for d in range(args.gpus)]
-    srv = Server(engines, Policy.srjf_calibrated())
+    srv = Server(engines, Policy.srjf_calibrated(), routing=args.routing)
     uvicorn.run(create_app(srv), host=args.host, port=args.port)
 
 

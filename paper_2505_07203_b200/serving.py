@@ -36,21 +36,48 @@ class ServingError(ValueError):
     """Invalid serving configuration or trace."""
 
 
+ROUTE_ROUND_ROBIN = "round_robin"
+ROUTE_LEAST_WORK = "least_work"
+
+
 @dataclass
 class Router:
-    """Sticky user -> instance assignment handed out round robin."""
+    """Sticky user -> instance assignment (ps/sim.py:52-66).
+
+    round_robin (default, the reference's parity mode): a first-seen user goes to the next instance in turn.
+    least_work (optional): a first-seen user goes to the instance with the least outstanding estimated
+    work (cache-miss tokens of its queued and running requests; ties to the lowest index), so a few heavy users do
+    not pile onto one GPU while another idles; later requests of the user stay there (its prefix is cached there).
+    The caller keeps `outstanding` up to date through add_work / done_work."""
 
     num_instances: int
     assignments: dict = field(default_factory=dict)
     next_rr: int = 0
+    mode: str = ROUTE_ROUND_ROBIN
+    outstanding: list = field(default_factory=list)
+
+    def __post_init__(self):
+        if self.mode not in (ROUTE_ROUND_ROBIN, ROUTE_LEAST_WORK):
+            raise ServingError(f"unknown routing mode {self.mode!r}")
+        if not self.outstanding:
+            self.outstanding = [0.0] * self.num_instances
 
     def route(self, request) -> int:
         inst = self.assignments.get(request.user_id)
         if inst is None:
-            inst = self.next_rr % self.num_instances
+            if self.mode == ROUTE_LEAST_WORK:
+                inst = min(range(self.num_instances), key=lambda i: (self.outstanding[i], i))
+            else:
+                inst = self.next_rr % self.num_instances
+                self.next_rr += 1
             self.assignments[request.user_id] = inst
-            self.next_rr += 1
         return inst
+
+    def add_work(self, inst: int, work: float):
+        self.outstanding[inst] += work
+
+    def done_work(self, inst: int, work: float):
+        self.outstanding[inst] -= work
 
 
 @dataclass(frozen=True)
@@ -134,9 +161,10 @@ ServiceFn = Callable[[int, WaitingRequest, int, list], object]
 
 
 def simulate(trace, num_instances: int, policy: Policy, capacity_tokens: int, service_fn: ServiceFn,
-             block_tokens: int = 16, jct_profile: JctProfile | None = None, max_input: int | None = None
-             ) -> ServeReport:
-    """Virtual-clock serving run (the reference's event loop with a pluggable service time)."""
+             block_tokens: int = 16, jct_profile: JctProfile | None = None, max_input: int | None = None,
+             routing: str = ROUTE_ROUND_ROBIN) -> ServeReport:
+    """Virtual-clock serving run (the reference's event loop with a pluggable service time). routing: the Router mode
+    (round_robin reproduces sim.run; least_work is the optional JCT-aware dispatcher)."""
     reqs = trace.requests
     arr = [r.arrival for r in reqs]
     if any(b < a for a, b in zip(arr, arr[1:])):
@@ -155,7 +183,8 @@ def simulate(trace, num_instances: int, policy: Policy, capacity_tokens: int, se
         return make_report([], [0.0] * num_instances, 0.0)
 
     insts = [Instance(PrefixCache(CacheConfig(capacity_tokens, block_tokens))) for _ in range(num_instances)]
-    router = Router(num_instances)
+    router = Router(num_instances, mode=routing)
+    work: dict = {}  # request id -> (instance, miss-token estimate) while queued or running (least_work routing)
     memo: dict = {}
     events: list = []
     seq = 0
@@ -189,6 +218,10 @@ def simulate(trace, num_instances: int, policy: Policy, capacity_tokens: int, se
             idx = router.route(r)
             inst = insts[idx]
             wr = WaitingRequest(request=r, arrival=now, chain=r.digest_chain(block_tokens, memo))
+            if routing == ROUTE_LEAST_WORK:
+                est = float(r.n_input - inst.cache.match_chain(wr.chain, committed=True))
+                work[r.id] = (idx, est)
+                router.add_work(idx, est)
             if policy.kind == POLICY_SRJF:
                 wr.frozen_jct = estimate_jct(r.n_input, inst.cache.match_chain(wr.chain, committed=True),
                                              policy.scoring, jct_profile)
@@ -203,6 +236,8 @@ def simulate(trace, num_instances: int, policy: Policy, capacity_tokens: int, se
         else:
             idx, wr, n_cached, started, adm, token = payload
             insts[idx].cache.commit(adm, now)
+            if routing == ROUTE_LEAST_WORK:
+                router.done_work(*work.pop(wr.request.id))
             records.append(RequestRecord(wr.request.id, wr.request.user_id, idx, wr.arrival, started, now,
                                          wr.request.n_input, n_cached, token))
     assert len(records) == len(reqs), "conservation violated"
@@ -505,12 +540,12 @@ class Server:
     """Request-level data parallelism over engines (one per GPU), SRJF-calibrated by default."""
 
     def __init__(self, engines: Sequence, policy: Policy | None = None, jct_profile: JctProfile | None = None,
-                 lookahead: bool = True):
+                 lookahead: bool = True, routing: str = ROUTE_ROUND_ROBIN):
         if not engines:
             raise ServingError("need at least one engine")
         self.policy = policy or Policy.srjf_calibrated()
         self.jct_profile = jct_profile
-        self.router = Router(len(engines))
+        self.router = Router(len(engines), mode=routing)
         self._t0 = time.monotonic()
         self._lock = threading.Lock()
         self.records: list = []
@@ -532,7 +567,8 @@ class Server:
     def submit(self, request, allowed: Sequence[int]) -> Future:
         """Queue one request (duck type .id, .user_id, .n_input, .tokens); resolves to a PrefillResult.
 
-        Thread-safe: routing (first-seen round robin) and the digest memo are updated under the server lock."""
+        Thread-safe: routing (first-seen round robin, or least outstanding work) and the digest memo are updated under
+        the server lock."""
         with self._lock:
             idx = self.router.route(request)
             bt = self.workers[idx].engine.block_tokens
@@ -540,6 +576,18 @@ class Server:
                 block_chain(request.tokens, bt)
         wr = WaitingRequest(request=request, arrival=self.clock(), chain=chain)
         fut: Future = Future()
+        if self.router.mode == ROUTE_LEAST_WORK:
+            w = self.workers[idx]
+            with w.cv:  # the worker thread owns the cache
+                est = float(request.n_input - w.inst.cache.match_chain(chain, committed=True))
+            with self._lock:
+                self.router.add_work(idx, est)
+
+            def _done(_f, idx=idx, est=est):
+                with self._lock:
+                    self.router.done_work(idx, est)
+
+            fut.add_done_callback(_done)
         self.workers[idx].enqueue(_Job(wr, tuple(allowed), fut), wr.arrival)
         return fut
 

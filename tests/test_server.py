@@ -189,3 +189,22 @@ def test_lookahead_decisions_match_oracle_when_all_queued():
         cache.insert_chain(w["chain"], t)
         t += 1.0
     assert order == expected
+
+
+def test_least_work_routing_serves_all_and_drains_the_estimates():
+    # the optional JCT-aware dispatcher in the wall-clock server: every request served, users sticky,
+    # and the outstanding-work counters back to zero once every future has resolved
+    from paper_2505_07203_b200.serving import ROUTE_LEAST_WORK
+
+    engines = [FakeEngine(), FakeEngine()]
+    srv = Server(engines, Policy.srjf_calibrated(), routing=ROUTE_LEAST_WORK)
+    try:
+        rep = replay(srv, wl.poisson_arrivals(small_trace(), 400.0, seed=1), [9642, 2822])
+    finally:
+        srv.close()
+    assert rep.served == 24
+    by_user = {}
+    for r in rep.records:
+        by_user.setdefault(r.user_id, set()).add(r.instance)
+    assert all(len(v) == 1 for v in by_user.values())
+    assert all(abs(x) < 1e-6 for x in srv.router.outstanding)
