@@ -121,6 +121,11 @@ def qwen32b(slo=30.0, model=None, repeats=10, grid=1000):
         res = refine_qps(res, slo, lambda q: run(wl.poisson_arrivals(trace, q, seed=0, keep_sessions=False)))
         fifo = sweep_rates(trace, rates, seed=0, keep_sessions=False,
                            run=lambda tr: simulate(tr, world, Policy.fifo(), cap, svc))
+        # the optional JCT-aware dispatcher: each (single-request) user to the replica with the least
+        # outstanding miss tokens instead of round robin
+        runl = lambda tr: simulate(tr, world, Policy.srjf_calibrated(), cap, svc, routing="least_work")  # noqa: E731
+        resl = sweep_rates(trace, rates, seed=0, run=runl, keep_sessions=False)
+        resl = refine_qps(resl, slo, lambda q: runl(wl.poisson_arrivals(trace, q, seed=0, keep_sessions=False)))
     best = qps_at_slo(res, slo)
     rep = dict(res)[best] if best else None
     return {"config": f"{M.name} ({'E4M3 W8A8' if M.weight_fp8 else 'bf16'}) random-init (64 L, 5120, 40/8 heads, "
@@ -130,6 +135,8 @@ def qwen32b(slo=30.0, model=None, repeats=10, grid=1000):
             "knee_found": bool(best) and any(r.p99_latency > slo for _, r in res),
             "prompt_tokens_per_s_at_slo": rep.prompt_tokens_per_s if rep else None,
             "fifo_qps_at_slo": qps_at_slo(fifo, slo),
+            "least_work_routing_qps_at_slo": qps_at_slo(resl, slo),
+            "least_work_sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency} for q, r in resl],
             "sweep": [{"rate": q, "p99_s": r.p99_latency, "mean_s": r.mean_latency} for q, r in res],
             "method": f"virtual-clock loop over 8 replicas (reference semantics, calibrated SRJF); service time of each "
                       f"request = a real forward on this GPU at its length rounded up to {grid} tokens "
