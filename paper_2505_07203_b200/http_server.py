@@ -16,8 +16,9 @@ generated token, chosen among the allowed ids):
                          "usage": {"prompt_tokens", "completion_tokens": 1, "prompt_tokens_details": {"cached_tokens"}}}
   GET  /v1/models
 
-No tokenizer assets are available offline: "prompt" text is encoded as its UTF-8 bytes (token id = byte),
-which is enough for prefix sharing to behave like real prompts; pass "tokens" for real tokenizer ids.
+Text prompts go through `--tokenizer PATH` (a local Hugging Face tokenizer directory, e.g. the model's own) when
+given; none ship offline, so by default "prompt" text is encoded as its UTF-8 bytes (token id = byte), which is
+enough for prefix sharing to behave like real prompts; pass "tokens" for real tokenizer ids.
 
   python -m paper_2505_07203_b200.http_server --gpus 1 --model llama-3.1-8b --port 8000
 """
@@ -65,12 +66,43 @@ except ImportError:  # pragma: no cover
     CompletionBody = None
 
 
+class ByteTokenizer:
+    """Offline stand-in: a prompt's UTF-8 bytes are its token ids; byte ids decode as their byte, others as <id>."""
+
+    def encode(self, text: str) -> list:
+        return list(text.encode("utf-8"))
+
+    def decode_one(self, tid: int) -> str:
+        return bytes([tid]).decode("latin-1") if 0 <= tid < 256 else f"<{tid}>"
+
+
+class HfTokenizer:
+    """A Hugging Face tokenizer loaded from local files (tokenizer.json / tokenizer.model directory, e.g. the
+    model's own): `--tokenizer PATH`. No special tokens are added, so a prompt's ids are exactly its text."""
+
+    def __init__(self, path: str):
+        from transformers import AutoTokenizer
+
+        self.tok = AutoTokenizer.from_pretrained(path, local_files_only=True)
+
+    def encode(self, text: str) -> list:
+        return list(self.tok.encode(text, add_special_tokens=False))
+
+    def decode_one(self, tid: int) -> str:
+        return self.tok.decode([tid])
+
+
+_TOKENIZER = ByteTokenizer()
+
+
 def _token_text(tid: int) -> str:
-    """Offline stand-in for detokenisation: byte ids decode as their byte, other ids as <id>."""
-    return bytes([tid]).decode("latin-1") if 0 <= tid < 256 else f"<{tid}>"
+    return _TOKENIZER.decode_one(tid)
 
 
-def create_app(server):
+def create_app(server, tokenizer=None):
+    global _TOKENIZER
+    if tokenizer is not None:
+        _TOKENIZER = tokenizer
     from fastapi import FastAPI, HTTPException
 
     from . import _lib
@@ -86,7 +118,7 @@ def create_app(server):
             raise HTTPException(400, "need tokens or prompt")
         if not body.allowed:
             raise HTTPException(400, "allowed must be non-empty")
-        raw = body.tokens if body.tokens is not None else list(body.prompt.encode("utf-8"))
+        raw = body.tokens if body.tokens is not None else _TOKENIZER.encode(body.prompt)
         if not raw:
             raise HTTPException(400, "empty prompt")
         if min(raw) < 0 or max(raw) >= 2 ** 32:
@@ -125,7 +157,7 @@ def create_app(server):
             allowed = [int(k) for k, v in body.logit_bias.items() if v >= 100]
         if not allowed:
             raise HTTPException(400, "give allowed_token_ids, or logit_bias with +100 on the allowed ids")
-        raw = body.prompt if isinstance(body.prompt, list) else list(body.prompt.encode("utf-8"))
+        raw = body.prompt if isinstance(body.prompt, list) else _TOKENIZER.encode(body.prompt)
         if not raw:
             raise HTTPException(400, "empty prompt")
         if min(raw) < 0 or max(raw) >= 2 ** 32:
@@ -171,6 +203,8 @@ def main():
     ap.add_argument("--max-tokens", type=int, default=32768)
     ap.add_argument("--host", default="127.0.0.1")
     ap.add_argument("--port", type=int, default=8000)
+    ap.add_argument("--tokenizer", default=None,
+                    help="local Hugging Face tokenizer directory for text prompts (default: UTF-8 bytes as ids)")
     ap.add_argument("--routing", default="round_robin", choices=["round_robin", "least_work"],
                     help="first-seen user placement across GPUs: the reference's round robin, or least outstanding "
                          "cache-miss work (SURVEY H9)")
@@ -183,7 +217,8 @@ def main():
 
     engines = [Engine(args.model, device=d, max_tokens=args.max_tokens) for d in range(args.gpus)]
     srv = Server(engines, Policy.srjf_calibrated(), routing=args.routing)
-    uvicorn.run(create_app(srv), host=args.host, port=args.port)
+    tok = HfTokenizer(args.tokenizer) if args.tokenizer else None
+    uvicorn.run(create_app(srv, tok), host=args.host, port=args.port)
 
 
 if __name__ == "__main__":

@@ -64,3 +64,26 @@ def test_openai_completions_surface():
         assert client.post("/v1/completions", json={"prompt": "a", "max_tokens": 1}).status_code == 400
     finally:
         srv.close()
+
+
+def test_custom_tokenizer_encodes_text_prompts():
+    # --tokenizer: text prompts go through the given tokenizer (a stand-in with the HfTokenizer interface here)
+    from paper_2505_07203_b200 import http_server as hs
+
+    class WordTok:
+        def encode(self, text):
+            return [1000 + len(w) for w in text.split()]
+
+        def decode_one(self, tid):
+            return f"w{tid}"
+
+    srv = Server([FakeEngine()], Policy.srjf_calibrated())
+    try:
+        client = TestClient(hs.create_app(srv, WordTok()))
+        r = client.post("/v1/completions", json={"model": "x", "prompt": "a bb ccc dddd", "max_tokens": 1,
+                                                 "allowed_token_ids": [9642, 2822]})
+        assert r.status_code == 200, r.text
+        assert r.json()["usage"]["prompt_tokens"] == 4
+    finally:
+        srv.close()
+        hs._TOKENIZER = hs.ByteTokenizer()
