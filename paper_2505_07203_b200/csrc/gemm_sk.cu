@@ -674,18 +674,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 // bf16 / fp32 (the prefix hit's gate/up), whose head fix-up streams the contributors' rows and leaves through staged
 // TMA stores. The cooperative fix-up of the residual / RoPE epilogues measured slower than the split-K reduce launches
 // (DESIGN.md "Short-M GEMMs").
-bool gemm_sk_enabled(int epi) {
+static int sk_mode() {  // 0: off, 1: every epilogue, 2 (default): SiLU.mul / bf16 / fp32
   static int mode = -1;
   if (mode < 0) {
     const char* v = getenv("PO_SK");
     mode = !v ? 2 : (v[0] == '1' ? 1 : 0);
   }
+  return mode;
+}
+bool gemm_sk_enabled(int epi) {
+  const int mode = sk_mode();
   if (mode == 1) return true;
   // (the residual epilogue's head fix-up - 3-5 contributors streamed per chunk, transposed residual boxes - measured
   // slower than swap + reduce on the hit's O / down: 1.12 vs 0.81 ms and 1.58 vs 1.29 ms per forward)
   return mode == 2 && (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32);
 }
-bool gemm_sk_enabled() { return gemm_sk_enabled(-1) || getenv("PO_SK") == nullptr; }
+bool gemm_sk_enabled() { return sk_mode() != 0; }
 
 size_t gemm_sk_ws_bytes() { return (size_t)num_sms() * 2 * 256 * 128 * sizeof(float); }
 size_t gemm_sk_flag_bytes() { return (size_t)num_sms() * 2 * SK_FLAG_STRIDE * sizeof(uint32_t); }
