@@ -599,13 +599,20 @@ def prefix_hit_roofline(eng, M, n, peaks):
         eng.prefill(toks, ALLOWED, nc, slots)
     ts = sorted(eng.prefill(toks, ALLOWED, nc, slots).service_s for _ in range(15))
     med = ts[len(ts) // 2]
+    # where a hit's time goes: CUDA events around every kernel class over 10 more hits (events break the PDL overlap,
+    # so the classes sum to more than the plain service time: compare shares)
+    eng.profile_begin()
+    for _ in range(10):
+        eng.prefill(toks, ALLOWED, nc, slots)
+    prof = eng.profile_end()
+    per_class = {k: {"ms_per_hit": ms / 10, "launches_per_hit": cnt // 10} for k, (ms, cnt) in prof.items() if cnt}
     lin_weights = M.weight_bytes - 2 * (2 * M.vocab * M.hidden)  # embedding / LM head rows are gathered, not streamed
     kv = M.kv_bytes_per_token[1] * n
     bytes_ = lin_weights + kv
     achieved = bytes_ / med / 1e9
     return {"n": n, "n_cached": nc, "service_ms_median": med * 1e3, "service_ms_min": ts[0] * 1e3,
             "bytes_per_request": bytes_, "achieved_gbs": achieved, "peak_gbs": peaks["hbm_gbs"],
-            "frac": achieved / peaks["hbm_gbs"], "bound": "hbm",
+            "frac": achieved / peaks["hbm_gbs"], "bound": "hbm", "per_class_events": per_class,
             "note": "algorithmic bytes = layer weights streamed once + cached K/V of all layers read once; "
                     "back-to-back hits (inside a mixed serving run the clocks are still recovering from cold "
                     "forwards: see qps_at_slo.measured_service_s.prefix_hit_median)"}
