@@ -37,9 +37,6 @@
 
 namespace po {
 
-#ifdef SK_ITER_TRACE
-__device__ long long g_sk_iter[64];
-#endif
 #ifdef SK_TRACE
 // globaltimer stamps per CTA of the last launch with N == SK_TRACE_N (tools/dbg_sk_trace.py): 0 start, 1 setup done,
 // 2 first full barrier (MMA), 3 last MMA commit, 4 first tfull (epilogue), 5 a dump published, 6 fix-up flags seen,
@@ -114,18 +111,8 @@ __device__ __forceinline__ void sk_rows(const GemmArgs& a, int row0, int nrows, 
                                         const int* slots, Src src) {
   const int lc = lane * 4;
   const int col = col0 + lc;
-#ifdef SK_ITER_TRACE
-  long long t_beg = clock64(), t_prev = t_beg, d_max = 0, d_first = -1;
-#endif
 #pragma unroll 4
   for (int i = wq; i < nrows; i += 4) {
-#ifdef SK_ITER_TRACE
-    {
-      const long long t = clock64();
-      if (i > wq) { d_max = max(d_max, t - t_prev); if (d_first < 0) d_first = t - t_prev; }
-      t_prev = t;
-    }
-#endif
     const int row = row0 + i;
     if constexpr (EPI == EPI_RESID_F32) {
       const float4 a4 = src(i, 0);
@@ -176,25 +163,13 @@ __device__ __forceinline__ void sk_rows(const GemmArgs& a, int row0, int nrows, 
         if (prow) *reinterpret_cast<uint2*>(prow + col) = v;
       }
     } else if constexpr (EPI == EPI_SILU_MUL) {
-#ifdef SK_NOSTORE
-      {
-        const float4 u = src(i, 0), w2 = src(i, 16);
-        if (u.x + w2.y == 12345.f) *static_cast<float*>(a.out) = u.z;
-      }
-#else
       if ((lc & 31) < 16) quad_epi<EPI>(a, row, col, src(i, 0), src(i, 16), s_inv[row], float4{});
-#endif
     } else if constexpr (EPI == EPI_F32) {
       *reinterpret_cast<float4*>(static_cast<float*>(a.out) + (long long)row * a.ldo + col) = src(i, 0);
     } else {
       quad_epi<EPI>(a, row, col, src(i, 0), float4{}, 1.f, float4{});
     }
   }
-#ifdef SK_ITER_TRACE
-  if (blockIdx.x < 4 && (threadIdx.x & 31) == 0 && a.N == 28672 && a.M > 1)
-    printf("blk %d warp %d rows %d: total %lld first %lld max %lld\n", blockIdx.x, threadIdx.x / 32, nrows,
-           clock64() - t_beg, d_first, d_max);
-#endif
 }
 
 template <int EPI>
@@ -640,9 +615,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       const SkCols kc = sk_cols<EPI>(args, col0 + lc, lc);
       const float* part = reinterpret_cast<const float*>(smem) + lc;
       const int pstride = (int)(bytes / 4);
-#ifdef SK_NOEPI
-      if (nr > 100000)
-#endif
       sk_rows<EPI>(args, r0, nr, wq, lane, col0, s_inv, kc, aux, 128, s_slot, [=](int i, int off) {
         const float* p = part + i * 128 + off;
         float4 v = *reinterpret_cast<const float4*>(p);
@@ -751,11 +723,6 @@ int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int e
 
 }  // namespace po
 
-#ifdef SK_ITER_TRACE
-extern "C" int po_debug_sk_iter(long long* h) {
-  return cudaMemcpyFromSymbol(h, po::g_sk_iter, sizeof(long long) * 64) == cudaSuccess ? 0 : -1;
-}
-#endif
 #ifdef SK_TRACE
 extern "C" int po_debug_swap_trace(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, po::g_sk_trace, sizeof(unsigned long long) * 296 * 16) == cudaSuccess ? 0 : -1;

@@ -35,8 +35,3 @@ for i, nm in enumerate(names):
 if len(sys.argv) > 1:
     for k, a in enumerate(arr):
         print(k, " ".join(f"{(x - t0) / 1e3:6.1f}" if x >= t0 else "   -  " for x in a[:16]))
-if True:
-    it = (ctypes.c_int64 * 64)()
-    _lib.load().po_debug_sk_iter(ctypes.addressof(it))
-    v = [x for x in it if x]
-    print("sk_rows iteration clocks (CTA 0 warp 4):", [v[k + 1] - v[k] for k in range(len(v) - 1)])
