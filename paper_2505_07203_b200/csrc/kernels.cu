@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
   float m = -FLT_MAX;
   int mi = 0x7fffffff;
   for (int a = threadIdx.x; a < n_allowed; a += blockDim.x) {
-    const float v = logits[a];
+    const float v = __ldcg(logits + a);  // other CTAs' rows: read at L2 (their fence + ticket ordered the stores)
     if (v > m || (v == m && a < mi)) { m = v; mi = a; }
   }
 #pragma unroll
@@ -207,9 +207,9 @@ __global__ void __launch_bounds__(1024) lm_head_kernel(const float* __restrict__
   __syncthreads();
   const float gm = bmax[0];
   float se = 0.f;
-  for (int a = threadIdx.x; a < n_allowed; a += blockDim.x) se += expf(logits[a] - gm);
+  for (int a = threadIdx.x; a < n_allowed; a += blockDim.x) se += expf(__ldcg(logits + a) - gm);
   se = block_sum(se, red);
-  for (int a = threadIdx.x; a < n_allowed; a += blockDim.x) probs[a] = expf(logits[a] - gm) / se;
+  for (int a = threadIdx.x; a < n_allowed; a += blockDim.x) probs[a] = expf(__ldcg(logits + a) - gm) / se;
   if (threadIdx.x == 0) *argmax = bidx[0];
 }
 // One CTA (32 warps, one allowed row each at a time) up to 256 rows: Yes/No lists are latency-bound and a single CTA
