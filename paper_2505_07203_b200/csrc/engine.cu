@@ -116,15 +116,17 @@ struct po_engine {
   int64_t pool_blocks = 0;
   int64_t weight_bytes = 0, arena_bytes = 0, pool_bytes = 0, free_after = 0, workspace_bytes = 0;
   std::vector<void*> allocs;
-  // persistent weight-streaming kernel (prefix hits): partial tiles, fix-up flags, grid-barrier counter
-  unsigned int* lm_ticket = nullptr;
+  unsigned int* lm_ticket = nullptr;      // multi-CTA LM head: CTAs finished (the last one runs the softmax)
   int* mlp_cnt = nullptr;                 // fused MLP launch: per-piece completion counters + exit ticket
   unsigned int* mlp_ticket = nullptr;
   int* mlp_next = nullptr;
-  int mlp_piece_max = 0;                  // rows per piece of the act ring (two pieces = chunk rows)  // multi-CTA LM head: CTAs finished (the last one runs the softmax)
+  int mlp_piece_max = 0;                  // rows per piece of the act ring (two pieces = chunk rows)
+  std::vector<int> piece_plan;            // MLP piece rows of the last planned row count (plan_mlp_pieces)
+  int piece_plan_rows = -1;
   float* sk_ws = nullptr;       // stream-K short-launch GEMMs: per-CTA partial slots and flags (gemm_sk.cu)
   uint32_t* sk_flags = nullptr;
   uint32_t sk_epoch = 0;
+  // persistent weight-streaming kernel (prefix hits): partial tiles, fix-up flags, grid-barrier counter
   float* stream_ws = nullptr;
   size_t stream_ws_bytes = 0;
   uint32_t* stream_flags = nullptr;
@@ -640,6 +642,62 @@ int po_load_weight(po_engine* e, int32_t kind, int32_t layer, const void* host, 
 }
 
 namespace {
+// MLP row pieces of a layer (each <= chunk rows; the act buffer holds one piece). The pair GEMMs run 256 x 256 tiles
+// over P = SMs / 2 pairs, so a piece of b 256-row blocks costs ceil(b * tiles_per_block / P) waves of each GEMM, a wave
+// taking time proportional to K. Equal row pieces (20,000 rows -> 3 x 6,667) round every piece up to whole blocks
+// and whole waves; here the ceil(rows / chunk) pieces take whole 256-row blocks (the last one the remainder rows)
+// split to minimise the summed wave cost of gate/up (K = hidden, 2I / 256 tiles per block) and down (K = I,
+// hidden / 256 tiles per block): 20,000 rows -> 4,352 + 7,936 + 7,712 (gate/up 26 + 47 + 47 waves instead of
+// 3 x 41). PO_PIECE_PLAN=0 keeps the equal pieces. Returns the piece row counts in launch order.
+void plan_mlp_pieces(int rows, int chunk, int hidden, int inter, int pairs, std::vector<int>& out) {
+  out.clear();
+  if (rows <= 0) return;
+  const int n_pieces = (rows + chunk - 1) / chunk;
+  static int mode = -1;
+  if (mode < 0) mode = (getenv("PO_PIECE_PLAN") && getenv("PO_PIECE_PLAN")[0] == '0') ? 0 : 1;
+  const int B = (rows + 255) / 256;
+  const int maxb = chunk / 256;
+  if (mode == 0 || n_pieces == 1 || chunk % 256 || maxb < 1 || pairs < 1 || (long long)n_pieces * maxb < B ||
+      n_pieces > 64 || B > 4096) {
+    const int piece = (rows + n_pieces - 1) / n_pieces;
+    for (int lo = 0; lo < rows; lo += piece) out.push_back(std::min(piece, rows - lo));
+    return;
+  }
+  const long long tgu = 2LL * inter / 256, tdn = hidden / 256;
+  auto cost = [&](int b) {
+    return (long long)hidden * ((b * tgu + pairs - 1) / pairs) + (long long)inter * ((b * tdn + pairs - 1) / pairs);
+  };
+  // best[k][u]: least cost of k pieces covering u blocks; pick[k][u]: the last piece's blocks
+  const long long INF = (1LL << 62);
+  std::vector<long long> best((size_t)(n_pieces + 1) * (B + 1), INF);
+  std::vector<int> pick((size_t)(n_pieces + 1) * (B + 1), 0);
+  best[0] = 0;
+  for (int k = 1; k <= n_pieces; ++k)
+    for (int u = 1; u <= B; ++u)
+      for (int b = 1; b <= maxb && b <= u; ++b) {
+        const long long prev = best[(size_t)(k - 1) * (B + 1) + u - b];
+        if (prev == INF) continue;
+        const long long c = prev + cost(b);
+        if (c < best[(size_t)k * (B + 1) + u]) {
+          best[(size_t)k * (B + 1) + u] = c;
+          pick[(size_t)k * (B + 1) + u] = b;
+        }
+      }
+  std::vector<int> blocks;
+  for (int k = n_pieces, u = B; k > 0; --k) {
+    const int b = pick[(size_t)k * (B + 1) + u];
+    blocks.push_back(b);
+    u -= b;
+  }
+  // whole blocks first, the remainder rows in the last piece
+  int done = 0;
+  for (size_t i = 0; i < blocks.size(); ++i) {
+    const int r = i + 1 < blocks.size() ? blocks[i] * 256 : rows - done;
+    out.push_back(r);
+    done += r;
+  }
+}
+
 // Validate a request and stage its block table; returns n_c (computed-from prefix) or a negative status.
 int stage_request(po_engine* e, int32_t n, int32_t n_cached, int32_t n_allowed, const int32_t* pool_block_ids,
                   int32_t n_blocks, int* n_admit_out) {
@@ -938,12 +996,14 @@ int forward(po_engine* e, const uint32_t* d_tok_miss, int n, int n_c, int n_admi
       if (l + 1 < L) rc |= qkv_gemm(l + 1);
       continue;
     }
-    // balanced chunks: ceil(rows / chunk) pieces of equal size (<= chunk), so no piece is a short tail whose GEMMs
-    // leave most SM pairs idle (20,000 rows at chunk 2304: nine pieces of 2,223 rows = 9 x 256-row tiles each)
-    const int n_pieces = (mlp_rows + c.chunk - 1) / c.chunk;
-    const int piece = n_pieces > 0 ? (mlp_rows + n_pieces - 1) / n_pieces : c.chunk;
-    for (int lo = row0; lo < n_miss && !rc; lo += piece) {
-      const int cr = (n_miss - lo) < piece ? (n_miss - lo) : piece;
+    // ceil(rows / chunk) pieces planned against the GEMMs' wave quantisation (plan_mlp_pieces)
+    if (e->piece_plan_rows != mlp_rows) {
+      plan_mlp_pieces(mlp_rows, c.chunk, h, I, po::num_sms() / 2, e->piece_plan);
+      e->piece_plan_rows = mlp_rows;
+    }
+    int lo = row0;
+    for (size_t pi = 0; pi < e->piece_plan.size() && !rc; lo += e->piece_plan[pi], ++pi) {
+      const int cr = e->piece_plan[pi];
       po::GemmArgs gu{};
       gu.M = cr; gu.N = 2 * I; gu.K = h; gu.a_row0 = lo;
       gu.out = e->act; gu.ldo = I; gu.split_ws = e->gemm_ws; gu.split_ws_bytes = e->gemm_ws_bytes;
