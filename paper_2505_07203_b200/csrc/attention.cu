@@ -333,6 +333,18 @@ __device__ unsigned long long g_attn_trace[TRACE_EVENTS * TRACE_TILES];
 #else
 #define TR(ev, j) do { } while (0)
 #endif
+// -DATTN_SPAN: globaltimer at entry, after setup, and at exit of every CTA (tools/attn_span.py), plus its split / unit
+#ifdef ATTN_SPAN
+__device__ unsigned long long g_attn_span[8192 * 4];
+__device__ __forceinline__ unsigned long long span_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPAN(i, v) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_attn_span[blockIdx.x * 4 + (i)] = (v); } while (0)
+#else
+#define SPAN(i, v) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_q,
@@ -359,6 +371,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = warp_id();
   const int lane = lane_id();
   if (threadIdx.x == 0) TR(21, 0);
+#ifdef ATTN_SPAN
+  SPAN(0, span_now());
+#endif
 
   // heaviest (longest causal extent) units first. Slot i of this CTA: head hs_i (first head of the kv group
   // when packed), first query position qs_i; rows_slot query rows per head in the slot.
@@ -405,6 +420,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int n_tiles = max(0, min(all_tiles, t0 + a.tiles_per_split) - t0);
 
   if (n_tiles == 0) return;  // a KV split past this query block's causal extent (uniform across the CTA)
+#ifdef ATTN_SPAN
+  SPAN(3, ((unsigned long long)split << 32) | (unsigned)unit);
+#endif
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&map);
@@ -417,6 +435,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TR(21, 1);
+#ifdef ATTN_SPAN
+  SPAN(1, span_now());
+#endif
   pdl_wait();     // qkv of this layer (QKV GEMM, pool gather) complete
   pdl_trigger();
   // registers move from the loader/MMA warpgroup (warps 8-11) to the two softmax warpgroups, which hold a
@@ -677,6 +698,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+#ifdef ATTN_SPAN
+  SPAN(2, span_now());
+#endif
 }
 
 // out[row, h, :] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s over the KV splits that exist for the row's block
@@ -860,6 +884,13 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
 }
 
 }  // namespace po
+
+#ifdef ATTN_SPAN
+extern "C" int po_debug_attn_span(unsigned long long* host, int n) {
+  if (n > 8192 * 4) n = 8192 * 4;
+  return cudaMemcpyFromSymbol(host, po::g_attn_span, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 #ifdef ATTN_TRACE
 extern "C" int po_debug_attn_trace(unsigned long long* host, int n) {
