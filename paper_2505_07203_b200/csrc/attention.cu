@@ -30,6 +30,9 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64
                       uint32_t box_inner, uint32_t box_outer);
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                       uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
+int make_tmap_4d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                      uint64_t stride1_bytes, uint64_t stride2_bytes, uint64_t stride3_bytes, uint32_t b0, uint32_t b1,
+                      uint32_t b2, uint32_t b3);
 
 namespace {
 constexpr int HD = 128;
@@ -72,6 +75,7 @@ struct AttnArgs {
   int pool_layer, pool_layers;  // map_pool block index = slot * pool_layers + pool_layer
   int pool_kcol, pool_vcol;     // column of this launch's K / V head 0 within a pool row
   int kv_band;                  // MODE_HEADS CTA order: kv heads per band (0 = all heads interleaved)
+  int pool_runs;                // map_run is valid: whole tiles in 8 consecutive slots load as two boxes
 };
 
 // Slot layouts. HEADS: two query heads of one GQA group over the same 128-row query block (K/V shared).
@@ -349,7 +353,7 @@ __device__ __forceinline__ unsigned long long span_now() {
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_pool, const __grid_constant__ CUtensorMap map16,
-                    const AttnArgs a) {
+                    const __grid_constant__ CUtensorMap map_run, const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sQ = smem;                       // 2 tiles
@@ -481,6 +485,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) {
           tma_load_2d_hint(dst, &map, bar, col, kr, keep);
           tma_load_2d_hint(dst + BOX_BYTES, &map, bar, col + 64, kr, keep);
+        }
+        return;
+      }
+      // a whole cached tile whose eight blocks sit in consecutive slots (the usual case: a request's prefix is
+      // admitted in order into free slots): two 128-row boxes over [slot][layer][16][kv_dim], as many TMA
+      // operations as a tile from qkv instead of sixteen 16-row boxes
+      const int s0 = __shfl_sync(0xffffffffu, cur, 0);
+      if (a.pool_runs && kr + BKV <= a.n_pool && __all_sync(0xffffffffu, cur == s0 + (lane & 7))) {
+        if (lane == 0) {
+          tma_load_4d_hint(dst, &map_run, bar, pcol, 0, a.pool_layer, s0, keep);
+          tma_load_4d_hint(dst + BOX_BYTES, &map_run, bar, pcol + 64, 0, a.pool_layer, s0, keep);
         }
         return;
       }
@@ -807,7 +822,7 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
                   cudaStream_t stream, void* workspace, size_t workspace_bytes, const AttnPool* pool) {
   if (hq % hkv) return -3;
   const AttnLayout lay = attention_layout(n_total, q_offset, hq, hkv);
-  CUtensorMap map, map_q, map_pool, map16;
+  CUtensorMap map, map_q, map_pool, map16, map_run;
   if (make_tmap_2d_bf16(&map, qkv, ld, n_total, ld * 2, 64, 128)) return -2;
   if (make_tmap_2d_bf16(&map_q, qkv, ld, n_total, ld * 2, 64, lay.R)) return -2;
   const bool use_pool = pool && pool->n_rows > 0;
@@ -817,10 +832,18 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
                           (uint64_t)pool->kv_dim * 2, (uint64_t)pool->kv_dim * 2 * 16, 64, 16, 1))
       return -2;
     if (make_tmap_2d_bf16(&map16, qkv, ld, n_total, ld * 2, 64, 16)) return -2;
+    map_run = map;
   } else {
     map_pool = map;
     map16 = map;
+    map_run = map;
   }
+  static int runs_env = -1;  // PO_POOL_RUNS=0: every pool tile as per-block boxes (A/B)
+  if (runs_env < 0) runs_env = (getenv("PO_POOL_RUNS") && getenv("PO_POOL_RUNS")[0] == '0') ? 0 : 1;
+  const bool pool_runs = use_pool && runs_env &&
+      make_tmap_4d_bf16(&map_run, pool->base, pool->kv_dim, 16, pool->num_layers, pool->num_blocks,
+                        (uint64_t)pool->kv_dim * 2, (uint64_t)pool->kv_dim * 2 * 16,
+                        (uint64_t)pool->kv_dim * 2 * 16 * pool->num_layers, 64, 16, 1, BKV / 16) == 0;
   ensure_smem_attr<attn_fwd_kernel>(SMEM_BYTES);
   AttnArgs a{};
   a.n_total = n_total;
@@ -853,6 +876,7 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
     a.kv_band = (lay.mode == MODE_HEADS && band > 0 && hkv % band == 0) ? band : 0;
   }
   if (use_pool) {
+    a.pool_runs = pool_runs ? 1 : 0;
     a.n_pool = pool->n_rows;
     a.pool_slots = pool->slots;
     a.pool_layer = pool->layer;
@@ -872,7 +896,8 @@ int attention_run(const void* qkv, long long ld, int n_total, int q_offset, int 
                                           (size_t)a.splits * a.n_q * hq * HD * sizeof(__nv_bfloat16));
   }
   const int grid = lay.ctas * a.splits;
-  launch_pdl(attn_fwd_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, stream, map, map_q, map_pool, map16, a);
+  launch_pdl(attn_fwd_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, stream, map, map_q, map_pool, map16, map_run,
+             a);
   if (a.splits > 1) {
     const long long total = (long long)a.n_q * hq * (HD / 4);
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);

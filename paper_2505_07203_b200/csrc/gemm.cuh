@@ -77,6 +77,9 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64
 // 3-D map (d0 innermost, 128B swizzle), e.g. the prefix pool [slot*layer][block_tokens][kv_dim].
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                       uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
+int make_tmap_4d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                      uint64_t stride1_bytes, uint64_t stride2_bytes, uint64_t stride3_bytes, uint32_t b0, uint32_t b1,
+                      uint32_t b2, uint32_t b3);
 int make_tmap_2d_epi(CUtensorMap* map, const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes,
                      bool swizzle128);
 int make_tmap_store_3d(CUtensorMap* map, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,

@@ -202,6 +202,42 @@ def test_pool_direct_straddling_tiles_match_oracle(tiny_engine, n_cached):
     check_against_oracle(TINY, warm, req, YES_NO, 42)
 
 
+def test_pool_slot_layouts_read_the_same_kv(tiny_engine):
+    """Pool-direct attention loads a whole cached 128-key tile whose eight blocks sit in consecutive slots as two
+    4-D boxes ([slot][layer][16][kv_dim]) and any other tile block by block. The same request cached under
+    consecutive, scattered and mixed slot layouts must give bit-identical hits, and match the oracle."""
+    bt = 16
+    base = tokens_for(23, 2000)
+    nb = len(base) // bt  # 125 blocks: 15 whole tiles + a partial one
+    n_cached = 1920
+    rng = np.random.default_rng(5)
+    pool = np.arange(260, 512)
+    mixed = []
+    for t in range((nb + 7) // 8):  # even tiles one consecutive run at a random start, odd tiles scattered
+        k = min(8, nb - 8 * t)
+        if t % 2 == 0:
+            start = 260 + 16 * t + int(rng.integers(0, 8))
+            mixed += list(range(start, start + k))
+        else:
+            mixed += [int(x) for x in rng.choice(pool[(pool >= 260 + 16 * t) & (pool < 260 + 16 * t + 16)], k,
+                                                 replace=False)]
+    layouts = {
+        "consecutive": list(range(300, 300 + nb)),
+        "scattered": [int(x) for x in rng.permutation(np.arange(300, 300 + nb))],
+        "mixed": mixed,
+    }
+    hits = {}
+    for name, slots in layouts.items():
+        assert len(set(slots)) == nb and all(0 <= x < 512 for x in slots)
+        tiny_engine.prefill(base, YES_NO, n_cached=0, pool_block_ids=slots)
+        ids = slots[: n_cached // bt] + [-1] * (nb - n_cached // bt)
+        hits[name] = tiny_engine.prefill(base, YES_NO, n_cached=n_cached, pool_block_ids=ids)
+        assert hits[name].n_cached == n_cached
+    for name in ("scattered", "mixed"):
+        assert np.array_equal(hits[name].logits, hits["consecutive"].logits), name
+    check_against_oracle(TINY, hits["mixed"], base, YES_NO, 42)
+
+
 @pytest.mark.parametrize("model", [TINY, SMALL], ids=["tiny", "small-splitk"])
 def test_short_suffix_admission_feeds_later_hits(model):
     """A prefix hit with a short miss suffix admits its suffix blocks from the QKV epilogue (the pair GEMM for the
