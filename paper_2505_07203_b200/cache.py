@@ -20,7 +20,6 @@ the reference's O(#leaves) scan; the chosen victims are identical (tests/test_ca
 from __future__ import annotations
 
 import heapq
-from collections import deque
 from dataclasses import dataclass, field
 from hashlib import blake2b
 from typing import Sequence
@@ -115,7 +114,10 @@ class PrefixCache:
         self._blocks: dict[bytes, _Node] = {}
         self._leaf_heap: list = []  # (last_use, ins_order, digest), lazily invalidated
         self._ins_counter = 0
-        self._free_slots = deque(range(config.capacity_blocks))
+        # free pool slots as a min-heap: admissions take the lowest free slots, so a request's new blocks (and the
+        # blocks of a chain evicted leaf by leaf and re-admitted) land in ascending consecutive slots, which
+        # pool-direct attention loads as whole-tile boxes (csrc/attention.cu)
+        self._free_slots = list(range(config.capacity_blocks))
         self._pending: Admission | None = None
         self.version = 0
 
@@ -196,10 +198,15 @@ class PrefixCache:
                 if victim is None:
                     break  # this block and the whole suffix are discarded
                 adm.evicted[victim[0]] = victim[1]
-            slot = self._add_block(d, chain[i - 1] if i > 0 else None, now)
-            adm.admit.append((i, slot))
+            self._add_block(d, chain[i - 1] if i > 0 else None, now, take_slot=False)
+            adm.admit.append((i, -1))
             adm.new_set.add(d)
             adm.stored_blocks = i + 1
+        # slots after the evictions: the admitted blocks take the lowest free slots in chain order (ascending runs)
+        for j, (i, _) in enumerate(adm.admit):
+            slot = heapq.heappop(self._free_slots)
+            self._blocks[chain[i]].slot = slot
+            adm.admit[j] = (i, slot)
         if adm.stored_blocks:
             d = chain[adm.stored_blocks - 1]
             self._stamp(d, self._blocks[d], now)
@@ -255,11 +262,11 @@ class PrefixCache:
         if node.children == 0:
             heapq.heappush(self._leaf_heap, (node.last_use, node.ins_order, d))
 
-    def _add_block(self, d: bytes, parent, now: float) -> int:
+    def _add_block(self, d: bytes, parent, now: float, take_slot: bool = True) -> int:
         self._ins_counter += 1
         if not self._free_slots:
             raise CacheError("prefix pool has no free slot")  # cannot happen: capacity checked first
-        slot = self._free_slots.popleft()
+        slot = heapq.heappop(self._free_slots) if take_slot else -1
         depth = 1 if parent is None else self._blocks[parent].depth + 1
         node = _Node(parent, depth, now, self._ins_counter, slot)
         self._blocks[d] = node
@@ -296,7 +303,7 @@ class PrefixCache:
 
     def _remove(self, d: bytes) -> _Node:
         node = self._blocks.pop(d)
-        self._free_slots.append(node.slot)
+        heapq.heappush(self._free_slots, node.slot)
         if node.parent is not None:
             p = self._blocks[node.parent]
             p.children -= 1

@@ -176,3 +176,23 @@ def test_config_validation():
         CacheConfig(capacity_tokens=16, block_tokens=0)
     with pytest.raises(CacheError):
         make(32).evict_to(64)
+
+
+def test_readmitted_blocks_take_ascending_consecutive_slots():
+    """Slots come from a min-heap and are handed out after an insertion's evictions: blocks admitted in place of a
+    chain evicted leaf by leaf (last block first) get ascending consecutive slots, so pool-direct attention can load
+    whole 8-block tiles as one box."""
+    c = make(64 * 16)
+    a = toks((0, 40 * 16))
+    b = toks((100000, 100000 + 40 * 16))
+    c.insert(a, now=0.0)
+    ca = block_chain(a, 16)
+    assert c.slots(ca, 40) == list(range(40))
+    c.insert(b, now=1.0)  # needs 16 of a's blocks: its tail 24..39 is evicted (last block first) while b is planned
+    cb = block_chain(b, 16)
+    sb = c.slots(cb, 40)
+    assert sb == list(range(24, 64))  # slots are handed out after the evictions, lowest first, in chain order
+    for t in range(5):
+        run = sb[8 * t: 8 * t + 8]
+        assert run == list(range(run[0], run[0] + 8))
+    c.check_invariants()
