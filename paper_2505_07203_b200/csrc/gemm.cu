@@ -8,6 +8,7 @@
 // Pipelines: smem full/empty ring (TMA <-> MMA) and TMEM full/empty pair (MMA <-> epilogue).
 #include "gemm.cuh"
 #include "gemm_epi.cuh"
+#include "stream.cuh"
 #include <cuda_fp8.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -465,8 +466,13 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
     if (i < total) {
       const int row = static_cast<int>(i / ncol4);
       const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
-      splitk_reduce_quad<EPI>(a, row, col, a.split_ws + (size_t)row * a.N + col, slice, a.k_splits,
-                              use ? s_sc[row - r_first] : -1.f);
+      int splits = a.k_splits;
+      const float* p = a.split_ws + (size_t)row * a.N + col;
+      if (a.sk_red) {  // stream-K partials: this column tile's contributors (gemm_sk.cu reduce mode)
+        const int t = col / 256;
+        splits = stream_owner(a.sk_w, a.sk_p, t * a.sk_nk + a.sk_nk - 1) - stream_owner(a.sk_w, a.sk_p, t * a.sk_nk) + 1;
+      }
+      splitk_reduce_quad<EPI>(a, row, col, p, slice, splits, use ? s_sc[row - r_first] : -1.f);
     }
     if (use) __syncthreads();  // s_sc is rewritten by the next iteration
   }

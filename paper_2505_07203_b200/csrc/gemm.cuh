@@ -59,6 +59,12 @@ struct GemmArgs {
   uint32_t sk_epoch;
   // tile raster of the row-major kernels: m-blocks per sweep over N (0 = the launcher's choice by K)
   int group_m;
+  // stream-K + reduce (gemm_sk.cu, sk_red = 1, opt-in PO_SK_RED=1): every segment's partial goes to split_ws slice j
+  // (its contributor index within the tile, k order) and splitk_reduce_kernel sums each tile's contributors of the
+  // equal-range stream-K split (sk_w work items, sk_p pairs, sk_nk k-blocks per tile)
+  int sk_red;
+  int sk_p, sk_nk;
+  long long sk_w;
 };
 
 struct GemmPlan {

@@ -318,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     const int et = threadIdx.x - 128;  // this thread's column of the CTA's 128 while draining TMEM
     const int lc = lane * 4;           // ... and its 4 columns in the row-major epilogue
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
-    if (EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) {
+    if ((EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE) && !args.sk_red) {
       // 1/rms of every activation row, once per launch: the rows' segment sums arrive by bulk copy (one L2 round
       // trip instead of a dependent chain per row), then each thread sums its rows in segment order (row_inv_rms)
       const int nseg = args.ss_nseg;
@@ -351,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     for (int f = lo; f < hi; ++it) {
       const SkSeg sg = sk_seg(f, hi, nk);
       f = sg.t * nk + sg.b;
-      const bool cut = sg.a > 0 || sg.b < nk;
+      const bool cut = args.sk_red || sg.a > 0 || sg.b < nk;  // reduce mode: every segment is a partial
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -360,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       const int col0 = sg.t * 256 + (int)rank * 128;  // the CTA's first output column of this tile
       const int slot = (int)blockIdx.x * 2 + (sg.t == first_t ? 0 : 1);  // dump slot of a cut segment
       const SkCols kc = cut ? SkCols{} : sk_cols<EPI>(args, col0 + lc, lc);
-      const bool head = HEADFIX && sg.a == 0 && sg.b < nk;  // HEADFIX: this pair finalises the cut tile
+      const bool head = HEADFIX && !args.sk_red && sg.a == 0 && sg.b < nk;  // HEADFIX: this pair finalises the cut tile
       const bool dump = cut && !head;
       int nq = 0;
       // HEADFIX: chunk k of the contributors' partials (their rows c0 .. c0+31, 16 KB each) into ring buffer k & 1
@@ -512,6 +512,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             continue;
           }
         }
+        if (args.sk_red) {
+          // contributor j of tile sg.t (k order) -> split_ws slice j ([maxc][M][N] fp32): this warp's 32 rows x 32
+          // columns staged transposed in shared memory, one TMA store (as the swap kernel's split-K partials)
+          const int j = pair - stream_owner(W, P, sg.t * nk);
+          uint8_t* wb = stg + (wq * 2 + (nch & 1)) * 4096;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer (two chunks ago) is done
+          __syncwarp();
+          float* tt = reinterpret_cast<float*>(wb);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) tt[i * 32 + lane] = __uint_as_float(r[i]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&map_st, wb, col0 + wq * 32, c0, j);
+            bulk_commit();
+          }
+          continue;
+        }
         if (cut) {  // the fp32 partial, straight from registers: one 128-byte line per warp and row
           float* dst = args.sk_ws + ((size_t)slot * 256 + c0) * 128 + et;
 #pragma unroll
@@ -538,7 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       named_bar_sync(1, 128);
       if (et == 0) {
         mbar_arrive_cluster(tempty0 + acc * 8);
-        if (dump) {  // publish the partial
+        if (dump && !args.sk_red) {  // publish the partial (the reduce launch needs no flag)
           st_release_u32(args.sk_flags + (size_t)slot * SK_FLAG_STRIDE, args.sk_epoch);
           SKT(5, true);
         }
@@ -550,7 +568,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     const SkSeg last = sk_seg(max(lo, (hi - 1) / nk * nk), hi, nk);
     uint32_t fx_phase = 0;
 #pragma unroll 1
-    for (int w = 0; w < (HEADFIX ? 0 : 2); ++w) {
+    for (int w = 0; w < ((HEADFIX || args.sk_red) ? 0 : 2); ++w) {
       const SkSeg sg = w == 0 ? first : last;
       if (w == 1 && last.t == first.t) break;
       if (sg.a == 0 && sg.b == nk) continue;  // a whole tile: done above
@@ -628,7 +646,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       named_bar_sync(1, 128);  // the copies of the next cut tile overwrite these rows
     }
     SKT(8, et == 0);
-    if (HEADFIX && et == 0) bulk_wait_all();  // TMA stores of the outputs complete before the CTA exits
+    // every warp's TMA stores (outputs, residual boxes, partials) complete before the CTA exits: bulk groups are
+    // per issuing thread, so each warp's lane 0 waits for its own
+    if ((HEADFIX || args.sk_red) && lane == 0) bulk_wait_all();
 
   }
 
@@ -654,14 +674,24 @@ static int sk_mode() {  // 0: off, 1: every epilogue, 2 (default): SiLU.mul / bf
   }
   return mode;
 }
+// PO_SK_RED=1 (opt-in, measured slower: DESIGN.md "Short-M GEMMs"): the residual / RoPE epilogues run stream-K with
+// every partial written to the split-K workspace and the split-K reduce kernel as the epilogue
+static bool sk_red_enabled() {
+  static int on = -1;
+  if (on < 0) on = (getenv("PO_SK_RED") && getenv("PO_SK_RED")[0] == '1') ? 1 : 0;
+  return on == 1;
+}
+static bool sk_red_epi(int epi) { return sk_mode() == 2 && sk_red_enabled() && (epi == EPI_RESID_F32 || epi == EPI_QKV_ROPE); }
 bool gemm_sk_enabled(int epi) {
   const int mode = sk_mode();
   if (mode == 1) return true;
+  if (sk_red_epi(epi)) return true;
   // (the residual epilogue's head fix-up - 3-5 contributors streamed per chunk, transposed residual boxes - measured
   // slower than swap + reduce on the hit's O / down: 1.12 vs 0.81 ms and 1.58 vs 1.29 ms per forward)
   return mode == 2 && (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32);
 }
 bool gemm_sk_enabled() { return sk_mode() != 0; }
+int splitk_reduce_launch(int epi, const GemmArgs& args, cudaStream_t stream);
 
 size_t gemm_sk_ws_bytes() { return (size_t)num_sms() * 2 * 256 * 128 * sizeof(float); }
 size_t gemm_sk_flag_bytes() { return (size_t)num_sms() * 2 * SK_FLAG_STRIDE * sizeof(uint32_t); }
@@ -677,6 +707,38 @@ int gemm_launch_sk(const CUtensorMap& map_w, const void* x, long long ldx, int e
   CUtensorMap map_x, map_st, map_r, map_xo;
   if (make_tmap_2d_bf16(&map_x, x, args.K, (uint64_t)args.a_row0 + args.M, ldx * 2, BK, np / 2)) return -2;
   map_st = map_r = map_xo = map_x;  // unused unless HEADFIX / RESID
+  if (sk_red_epi(epi)) {
+    // stream-K + reduce: each tile's contributors write slices 0 .. c-1 of split_ws, then the split-K reduce kernel
+    // sums them in k order and runs the epilogue
+    const int nk = args.K / BK;
+    int maxc = 1;
+    for (int t = 0; t < args.N / 256; ++t)
+      maxc = std::max(maxc, stream_owner(W, P, t * nk + nk - 1) - stream_owner(W, P, t * nk) + 1);
+    if (!args.split_ws || (size_t)maxc * args.M * args.N * sizeof(float) > args.split_ws_bytes) return 1;
+    if (make_tmap_store_3d(&map_st, args.split_ws, true, args.N, args.M, maxc, (uint64_t)args.N * 4,
+                           (uint64_t)args.N * args.M * 4, 32, 32))
+      return 1;
+    args.sk_red = 1;
+    args.sk_w = W;
+    args.sk_p = P;
+    args.sk_nk = nk;
+    switch (epi) {
+      case EPI_RESID_F32:
+        ensure_smem_attr<gemm_sk_kernel<EPI_RESID_F32>>(SMEM);
+        launch_pdl(gemm_sk_kernel<EPI_RESID_F32>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, map_st, map_r,
+                   map_xo, args, np);
+        break;
+      case EPI_QKV_ROPE:
+        ensure_smem_attr<gemm_sk_kernel<EPI_QKV_ROPE>>(SMEM);
+        launch_pdl(gemm_sk_kernel<EPI_QKV_ROPE>, dim3(2 * P), dim3(NT), SMEM, stream, map_w, map_x, map_st, map_r,
+                   map_xo, args, np);
+        break;
+      default: return 1;
+    }
+    if (cudaGetLastError() != cudaSuccess) return -4;
+    return splitk_reduce_launch(epi, args, stream);
+  }
+  args.sk_red = 0;
   if (epi == EPI_SILU_MUL || epi == EPI_BF16 || epi == EPI_F32 || epi == EPI_RESID_F32) {
     // HEADFIX: the head pair streams the other contributors' rows through two halves of its stage ring, 32 rows
     // (16 KB) per contributor per chunk
