@@ -2,6 +2,7 @@
 read once per process):
   * PO_SK=1: stream-K short-launch GEMMs (csrc/gemm_sk.cu) - the short-M GEMM tests (fp32 torch reference of each
     epilogue) and the engine tests (CPU oracle: argmax identical, logits within the bf16 tolerance);
+  * PO_SK_RED=1: stream-K with split-K-reduce epilogues for the residual / RoPE short launches - the same tests;
   * PO_FUSED_MLP=1: the fused per-layer MLP launch (csrc/mlp.cu) - the engine tests (including the bit-exact chunk
     invariance across 512 / 1024 / 8192-row chunks) and the Llama-3.1-8B-dims oracle fixtures."""
 
@@ -30,6 +31,11 @@ def test_stream_k_short_gemms():
 
 def test_stream_k_engine_against_oracle():
     _run(["tests/test_gpu_engine.py", "tests/test_gpu_parity_fullsize.py"], PO_SK="1")
+
+
+def test_stream_k_reduce_mode():
+    _run(["tests/test_gpu_gemm.py", "-k", "swap or splitk"], PO_SK_RED="1")
+    _run(["tests/test_gpu_engine.py", "tests/test_gpu_parity_fullsize.py"], PO_SK_RED="1")
 
 
 def test_fused_mlp_engine_against_oracle():
