@@ -387,7 +387,8 @@ int po_init(int32_t device, const po_model_cfg* cfg, uint64_t seed, po_engine** 
   {
     // split-KV workspace: largest need over query lengths that trigger splitting, at n_total = max_tokens
     size_t ws = 0;
-    for (int nq = 1; nq <= 148 * 128 && nq <= T; nq += 64)
+    // (every query length: the need is splits x n_q, largest at the top of each constant-split band)
+    for (int nq = 1; nq <= 148 * 128 && nq <= T; ++nq)
       ws = std::max(ws, po::attention_workspace_bytes((int)T, (int)T - nq, c.n_heads, c.n_kv_heads));
     e->attn_ws_bytes = ws;
     if (ws && dalloc(e, &e->attn_ws, ws, &e->workspace_bytes))
