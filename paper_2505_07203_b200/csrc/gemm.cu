@@ -429,12 +429,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
   }
 }
 
-template <int EPI>
-__global__ void splitk_reduce_kernel(const GemmArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  const int ncol4 = a.N / 4;
-  const long long total = (long long)a.M * ncol4;
+// Grid-stride loop over output quads; IDX = int when M * N / 4 fits (32-bit row/column divisions: the 64-bit ones are
+// a ~70-instruction software sequence each, three per quad, in a kernel that is issue-bound at short M)
+template <int EPI, typename IDX>
+__device__ __forceinline__ void splitk_reduce_loop(const GemmArgs& a, IDX total, IDX ncol4) {
   const size_t slice = (size_t)a.M * a.N;
   constexpr bool NORM = EPI == EPI_SILU_MUL || EPI == EPI_QKV_ROPE;
   // folded-norm consumers: the 1/rms of the block's rows (a block's quads span few rows) is computed once per row by
@@ -443,10 +441,10 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
   __shared__ float s_ss[8][64];
   __shared__ float s_sc[8];
   const bool share = NORM && a.ss_in && a.ss_nseg <= 64;
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < total; base += (long long)gridDim.x * blockDim.x) {
-    const long long i = base + threadIdx.x;
+  for (IDX base = (IDX)blockIdx.x * blockDim.x; base < total; base += (IDX)gridDim.x * blockDim.x) {
+    const IDX i = base + threadIdx.x;
     const int r_first = static_cast<int>(base / ncol4);
-    const long long last = base + blockDim.x - 1 < total ? base + blockDim.x - 1 : total - 1;
+    const IDX last = base + (IDX)blockDim.x - 1 < total ? base + (IDX)blockDim.x - 1 : total - 1;
     const int nrows = static_cast<int>(last / ncol4) - r_first + 1;
     const bool use = share && nrows <= 8;  // uniform across the block
     if (use) {
@@ -457,7 +455,8 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
         __syncwarp();
         if (ln == 0) {
           float sum = 0.f;
-          for (int k = 0; k < a.ss_nseg; ++k) sum += s_ss[w][k];
+#pragma unroll 16
+          for (int k = 0; k < a.ss_nseg; ++k) sum += s_ss[w][k];  // loads batched ahead of the in-order adds
           s_sc[w] = rsqrtf(sum / a.norm_dim + a.norm_eps);
         }
       }
@@ -465,7 +464,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
     }
     if (i < total) {
       const int row = static_cast<int>(i / ncol4);
-      const int col = static_cast<int>(i - (long long)row * ncol4) * 4;
+      const int col = static_cast<int>(i - (IDX)row * ncol4) * 4;
       int splits = a.k_splits;
       const float* p = a.split_ws + (size_t)row * a.N + col;
       if (a.sk_red) {  // stream-K partials: this column tile's contributors (gemm_sk.cu reduce mode)
@@ -474,8 +473,20 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
       }
       splitk_reduce_quad<EPI>(a, row, col, p, slice, splits, use ? s_sc[row - r_first] : -1.f);
     }
-    if (use) __syncthreads();  // s_sc is rewritten by the next iteration
+    if (use) __syncthreads();  // s_ss / s_sc are rewritten by the next iteration
   }
+}
+
+template <int EPI>
+__global__ void splitk_reduce_kernel(const GemmArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const long long ncol4 = a.N / 4;
+  const long long total = (long long)a.M * ncol4;
+  if (total + 2LL * 148 * 8 * 256 < 0x7fffffffLL)  // base + stride stays below 2^31 too
+    splitk_reduce_loop<EPI, int>(a, (int)total, (int)ncol4);
+  else
+    splitk_reduce_loop<EPI, long long>(a, total, ncol4);
 }
 
 int splitk_reduce_launch(int epi, const GemmArgs& args, cudaStream_t stream) {

@@ -259,16 +259,22 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tad
 }
 
 
-// Sum of the k-split partials at p, p + slice, ... in split order; all loads issued before the adds.
+// Sum of the k-split partials at p, p + slice, ... in split order; the loads of each group of four issued before its
+// adds. Group width 4 and pointer increments (not 8 predicated slots with 64-bit index products): the reduce launches
+// of short-M GEMMs are issue-bound, and 3-6 splits are the usual counts.
 __device__ __forceinline__ float4 split_sum(const float* p, size_t slice, int splits) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s0 = 0; s0 < splits; s0 += 8) {
-    float4 v[8];
+  const float4* q = reinterpret_cast<const float4*>(p);
+  const size_t step = slice / 4;  // slice is a multiple of 4 floats (N % 4 == 0)
+  for (int s0 = 0; s0 < splits; s0 += 4) {
+    float4 v[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      v[k] = s0 + k < splits ? __ldcg(reinterpret_cast<const float4*>(p + (s0 + k) * slice)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < 4; ++k) {
+      v[k] = s0 + k < splits ? __ldcg(q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      q += step;
+    }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
       if (s0 + k < splits) {
         acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
       }
