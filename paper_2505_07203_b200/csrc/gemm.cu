@@ -429,6 +429,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EW>(), 
   }
 }
 
+// Work units of a reduce row: one per output quad, except that a RoPE unit covers a quad of a head's first 64 columns
+// together with its rotation partner at +64, and a SiLU.mul unit a gate quad together with its up quad at +16, so no
+// lane of a warp idles on the partner columns (the kernel is issue-bound at short M).
+__host__ __device__ __forceinline__ int reduce_units_per_row(int epi, int N, int rope_cols) {
+  return epi == EPI_QKV_ROPE ? rope_cols / 8 + (N - rope_cols) / 4 : epi == EPI_SILU_MUL ? N / 8 : N / 4;
+}
+template <int EPI>
+__device__ __forceinline__ int reduce_unit_col(const GemmArgs& a, int u) {
+  if constexpr (EPI == EPI_QKV_ROPE) {
+    const int ru = a.rope_cols / 8;
+    return u < ru ? (u >> 4) * 128 + (u & 15) * 4 : a.rope_cols + (u - ru) * 4;
+  } else if constexpr (EPI == EPI_SILU_MUL) {
+    return (u >> 2) * 32 + (u & 3) * 4;
+  } else {
+    return u * 4;
+  }
+}
+
 // Grid-stride loop over output quads; IDX = int when M * N / 4 fits (32-bit row/column divisions: the 64-bit ones are
 // a ~70-instruction software sequence each, three per quad, in a kernel that is issue-bound at short M)
 template <int EPI, typename IDX>
@@ -464,7 +482,7 @@ __device__ __forceinline__ void splitk_reduce_loop(const GemmArgs& a, IDX total,
     }
     if (i < total) {
       const int row = static_cast<int>(i / ncol4);
-      const int col = static_cast<int>(i - (IDX)row * ncol4) * 4;
+      const int col = reduce_unit_col<EPI>(a, static_cast<int>(i - (IDX)row * ncol4));
       int splits = a.k_splits;
       const float* p = a.split_ws + (size_t)row * a.N + col;
       if (a.sk_red) {  // stream-K partials: this column tile's contributors (gemm_sk.cu reduce mode)
@@ -481,7 +499,7 @@ template <int EPI>
 __global__ void splitk_reduce_kernel(const GemmArgs a) {
   pdl_wait();
   pdl_trigger();
-  const long long ncol4 = a.N / 4;
+  const long long ncol4 = reduce_units_per_row(EPI, a.N, a.rope_cols);  // units per row
   const long long total = (long long)a.M * ncol4;
   if (total + 2LL * 148 * 8 * 256 < 0x7fffffffLL)  // base + stride stays below 2^31 too
     splitk_reduce_loop<EPI, int>(a, (int)total, (int)ncol4);
@@ -490,7 +508,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs a) {
 }
 
 int splitk_reduce_launch(int epi, const GemmArgs& args, cudaStream_t stream) {
-  const long long total = (long long)args.M * (args.N / 4);
+  const long long total = (long long)args.M * reduce_units_per_row(epi, args.N, args.rope_cols);
   const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
   switch (epi) {
     case EPI_BF16: launch_pdl(splitk_reduce_kernel<EPI_BF16>, dim3(blocks), dim3(256), 0, stream, args); break;
@@ -696,7 +714,7 @@ static int launch_pair_t(const CUtensorMap& map_a, const CUtensorMap& map_b2, co
   launch_pdl(gemm2_kernel<EPI, BNT, F8>, dim3(2 * npairs), dim3(pair_threads<pair_ew<F8, BNT>()>()),
              pair_smem<EPI, BNT, F8>(), stream, map_a, map_b2, map_r, map_xo, args);
   if (args.k_splits > 1) {
-    const long long total = (long long)args.M * (args.N / 4);
+    const long long total = (long long)args.M * reduce_units_per_row(EPI, args.N, args.rope_cols);
     const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
     launch_pdl(splitk_reduce_kernel<EPI>, dim3(blocks), dim3(256), 0, stream, args);
   }
@@ -759,7 +777,7 @@ static int launch(const CUtensorMap& map_a, const CUtensorMap& map_b, const Gemm
   const int grid = tiles < num_sms() ? tiles : num_sms();
   launch_pdl(gemm_kernel<EPI>, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, stream, map_a, map_b, args);
   if (args.k_splits > 1) {
-    const long long total = (long long)args.M * (args.N / 4);
+    const long long total = (long long)args.M * reduce_units_per_row(EPI, args.N, args.rope_cols);
     const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
     launch_pdl(splitk_reduce_kernel<EPI>, dim3(blocks), dim3(256), 0, stream, args);
   }
