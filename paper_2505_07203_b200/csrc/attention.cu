@@ -724,32 +724,54 @@ __global__ void attn_combine_kernel(const __nv_bfloat16* __restrict__ part_o, co
                                     __nv_bfloat16* __restrict__ out, long long ldo) {
   pdl_wait();
   pdl_trigger();
-  const long long total = (long long)n_q * hq * (HD / 4);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int q4 = static_cast<int>(i % (HD / 4));
-    const long long rh = i / (HD / 4);
-    const int h = static_cast<int>(rh % hq);
-    const int row = static_cast<int>(rh / hq);
+  // 32-bit indices (n_q * hq * 32 < 2^31 for any split launch: n_q <= 148 * 128): 64-bit divisions by hq are a
+  // ~70-instruction software sequence each
+  const int total = n_q * hq * (HD / 4);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int q4 = i % (HD / 4);
+    const int rh = i / (HD / 4);
+    const int h = rh % hq;
+    const int row = rh / hq;
     const int q_hi = min(q_offset + (row / span) * span + span - 1, n_total - 1);
     const int all_tiles = q_hi / BKV + 1;
     const int ns = min(splits, (all_tiles + tiles_per_split - 1) / tiles_per_split);
+    // split s of (row, h) at ml + s * stride, its O quad at o + s * stride * HD / 4 (pointer increments)
+    const int rh_idx = row * hq + h;
+    const size_t stride = (size_t)n_q * hq;
+    const float2* ml = part_ml + rh_idx;
+    const uint2* o4 = reinterpret_cast<const uint2*>(part_o) + (size_t)rh_idx * (HD / 4) + q4;
     float M = -INFINITY;
-    for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[((long long)s * n_q + row) * hq + h].x);
+    {
+      const float2* mp = ml;
+#pragma unroll 4
+      for (int s = 0; s < ns; ++s, mp += stride) M = fmaxf(M, mp->x);
+    }
     float L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < ns; ++s) {
-      const float2 ml = part_ml[((long long)s * n_q + row) * hq + h];
-      const float w = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
-      L += w * ml.y;
-      const uint2 ob = reinterpret_cast<const uint2*>(part_o + ((long long)s * n_q + row) * hq * HD + h * HD)[q4];
-      const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ob.x));
-      const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ob.y));
-      const float4 o = make_float4(o01.x, o01.y, o23.x, o23.y);
-      acc.x += w * o.x;
-      acc.y += w * o.y;
-      acc.z += w * o.z;
-      acc.w += w * o.w;
+    for (int s0 = 0; s0 < ns; s0 += 4) {
+      // a group's (m, l) and O loads issued together, then the in-order weighted sums
+      float2 mls[4];
+      uint2 obs[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mls[k] = s0 + k < ns ? *ml : make_float2(-INFINITY, 0.f);
+        obs[k] = s0 + k < ns ? *o4 : make_uint2(0u, 0u);
+        ml += stride;
+        o4 += stride * (HD / 4);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (s0 + k < ns) {
+          const float w = mls[k].x == -INFINITY ? 0.f : exp2f(mls[k].x - M);
+          L += w * mls[k].y;
+          const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&obs[k].x));
+          const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&obs[k].y));
+          acc.x += w * o01.x;
+          acc.y += w * o01.y;
+          acc.z += w * o23.x;
+          acc.w += w * o23.y;
+        }
+      }
     }
     const float inv = 1.0f / L;
     reinterpret_cast<uint2*>(out + (long long)row * ldo + h * HD)[q4] =
